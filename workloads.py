@@ -1,0 +1,85 @@
+"""Seeded synthetic workloads (INPUTS ONLY — no SRMDP arithmetic here).
+
+Shared by tests/, bench.py and __graft_entry__.smoke(): the oracle and the
+CUDA path each turn these plain dicts into their own problem objects.
+Shapes follow BASELINE.json ``configs`` and SURVEY.md §8(d); the problem
+families follow the paper's §5.1 benchmark and the
+closed-form cases of DESIGN.md §Inputs.
+
+Parameter layouts (docs/streams.md §7 and include/srmdp.h):
+  dyn "bm": none; "gbm": [mu_0..mu_{d-1}, s_0..s_{d-1}];
+  "affine": [b0 (d), B1 (d*d row-major), S0 (d*q row-major)]
+  f "zero": none; "linear": [a, c, theta_0..theta_{q-1}]  (f = a y + theta.z + c);
+  "paper": none  ((sum z)(y - (2+q)/(2q)))
+  g "affine": [a, w_0..w_{d-1}]; "paper": none (omega/(1+omega))
+"""
+from __future__ import annotations
+
+import math
+
+
+def paper_local_lipschitz(q: int) -> float:
+    """Local L_f of the §5.1 driver on |y|<=1, |z_k|<=1 (reading R5)."""
+    return max(q / 4.0, math.sqrt(q) * (0.5 + 1.0 / q))
+
+
+def cfg1(seed: int = 1, M: int = 256) -> dict:
+    """d=q=1, X=W, f=0, affine g, N=4, #C=10, M=256 (BASELINE configs[0])."""
+    return dict(name="cfg1", d=1, q=1, N=4, T=1.0, dyn="bm", f="zero", g="affine",
+                g_params=[0.5, 0.25], C=10, L=6.5, mu=1.0, M=M,
+                C_y_override=math.inf, C_z_override=math.inf, seed=seed)
+
+
+def cfg2(seed: int = 1, M: int = 1024, N: int = 10, C: int = 20) -> dict:
+    """d=q=2 Black-Scholes-type linear driver, GBM, N=10, 20^2 cells, M=1024 (configs[1])."""
+    mu, s, r = 0.05, 0.2, 0.03
+    theta = (mu - r) / s
+    return dict(name="cfg2", d=2, q=2, N=N, T=1.0, dyn="gbm",
+                dyn_params=[mu, mu, s, s], f="linear", f_params=[-r, 0.0, -theta, -theta],
+                g="affine", g_params=[1.0, 1.0, 1.0], C=C, L=6.5, mu=1.0, M=M,
+                C_y_override=math.inf, C_z_override=math.inf, seed=seed,
+                bs=dict(mu=mu, s=s, r=r, a=1.0, w=[1.0, 1.0]))
+
+
+def benchmark(d: int, N: int, C: int, M: int, seed: int = 1, name: str = "bench") -> dict:
+    """§5.1 benchmark: X=W, d=q, T=1, mu=1, L=6.5, C_g=1, C_f=0."""
+    return dict(name=name, d=d, q=d, N=N, T=1.0, dyn="bm", f="paper", g="paper",
+                C=C, L=6.5, mu=1.0, M=M, C_g=1.0, C_f=0.0, L_f=paper_local_lipschitz(d),
+                seed=seed)
+
+
+def cfg3(seed: int = 1, M: int = 2048) -> dict:
+    """d=4 benchmark, N=20, 10^4 cells, M=2048 (configs[2])."""
+    return benchmark(4, 20, 10, M, seed, "cfg3")
+
+
+def cfg4(seed: int = 1, M: int = 4096) -> dict:
+    """d=6 benchmark, N=30, 5^6 cells, M=4096 (configs[3]) — the bench workload."""
+    return benchmark(6, 30, 5, M, seed, "cfg4")
+
+
+def cfg5(seed: int = 1, M: int = 3200) -> dict:
+    """d=19 benchmark, N=5, 2^19 cells, M=3200 (paper row P:1259; configs[4])."""
+    return benchmark(19, 5, 2, M, seed, "cfg5")
+
+
+def bookkeeping(d: int = 2, N: int = 5, C: int = 4, M: int = 64, seed: int = 7,
+                beta=None, r: float = 0.1, a: float = 0.3, w=None) -> dict:
+    """sigma=0, constant drift beta, f = r y, g = a + w.x (closed form)."""
+    beta = list(beta) if beta is not None else [0.9 * (l + 1) for l in range(d)]
+    w = list(w) if w is not None else [0.5 - 0.2 * l for l in range(d)]
+    q = d
+    dyn = beta + [0.0] * (d * d) + [0.0] * (d * q)
+    return dict(name="bookkeeping", d=d, q=q, N=N, T=1.0, dyn="affine", dyn_params=dyn,
+                f="linear", f_params=[r, 0.0] + [0.0] * q, g="affine", g_params=[a] + w,
+                C=C, L=2.0, mu=1.0, M=M, C_y_override=math.inf, C_z_override=math.inf,
+                seed=seed, bk=dict(beta=beta, r=r, a=a, w=w))
+
+
+CONFIGS = {"cfg1": cfg1, "cfg2": cfg2, "cfg3": cfg3, "cfg4": cfg4, "cfg5": cfg5}
+
+
+def path_steps(w: dict) -> int:
+    """K*M*N(N+1)/2 — the metric's unit."""
+    K = w["C"] ** w["d"]
+    return K * w["M"] * w["N"] * (w["N"] + 1) // 2
