@@ -1,0 +1,335 @@
+"""bench.py — SRMDP backward-sweep throughput on B200 (one JSON line on rank 0).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl srmdp|reference] [--config cfg4]
+
+A "step" is one full SRMDP solve (Alg. srmdp: all N time
+points, every hypercube, every path) of the synthetic workload (default cfg4 =
+BASELINE.json configs[3]: §5.1 benchmark d=q=6, N=30, #C=5 -> K=15625, M=4096).
+metric = simulated path-steps/s = K*M*N(N+1)/2 per solve / seconds.
+
+Timing: W warm-up solves, then K solves each bracketed by CUDA events on the
+library's stream, L2 flushed (256 MB write) before every timed solve outside
+the events; barrier + synchronize on both sides; max over ranks. For N>1 the
+driver launches this under torchrun; the library shards cells over ranks and
+all-gathers every step's coefficients with NCCL (strong scaling of a fixed
+problem). `--impl reference` times the CPU oracle (test infrastructure) on a
+bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import workloads  # noqa: E402
+
+
+# ----------------------------------------------------------------------------
+# algorithmic FP64 work per unit (counts follow the
+# operation sequences of docs/streams.md and docs/detmath.md; fma = 2 flops,
+# add/mul/div/sqrt = 1)
+# ----------------------------------------------------------------------------
+F_PAIR = 77          # one Box-Muller pair: 2 u01 + dm_log 31 + (-2*, sqrt) 2 + dm_sincospi2 38 + scaling 4
+F_COORD = 38         # one conditional-logistic coordinate: u01 1 + inverse CDF 6 + dm_log 31
+
+
+def flops_per_path_step(w):
+    d, q = w["d"], w["q"]
+    euler = {"bm": d, "gbm": 5 * d, "affine": d * (2 * d + 2 * q + 2)}[w["dyn"]]
+    return F_PAIR * math.ceil(q / 2) + euler + 3 * d + 2 * (q + 1) * (d + 1) + 2 * q + 4
+
+
+def flops_per_path_start(w):
+    d, q = w["d"], w["q"]
+    return (F_COORD * d + d + 2 * q + (d + 1) * (d + 2) + 2 * q * (d + 1)
+            + 2 * q * (d + 1) + 2 * q + 4 + 2 * (d + 1) + (d + 3))
+
+
+def algorithmic_flops(w):
+    K = w["C"] ** w["d"]
+    steps = K * w["M"] * w["N"] * (w["N"] + 1) // 2
+    starts = K * w["M"] * w["N"]
+    return flops_per_path_step(w) * steps + flops_per_path_start(w) * starts
+
+
+def fp64_peak():
+    """Roofline denominator: MEASURED_PEAKS.json if it has FP64, else our
+    measured DFMA microbenchmark (profiles/), else the derivation from unit
+    counts and the max clock (148 SM x 64 FP64 lanes x 2 x 1.965 GHz)."""
+    try:
+        mp = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        for k in ("fp64_tflops_sustained", "fp64_tflops"):
+            if k in mp:
+                return float(mp[k]), "MEASURED_PEAKS.json:" + k
+    except Exception:
+        pass
+    try:
+        m = json.load(open(os.path.join(ROOT, "profiles", "fp64_peak.json")))
+        return float(m["fp64_tflops_sustained"]), "measured DFMA microbenchmark (profiles/fp64_peak.json, sustained)"
+    except Exception:
+        pass
+    return 148 * 64 * 2 * 1.965e9 / 1e12, "derived: 148 SM x 64 FP64 FMA/clk x 2 x 1.965 GHz"
+
+
+def ncu_traffic():
+    try:
+        return json.load(open(os.path.join(ROOT, "profiles", "step_kernel_traffic.json")))
+    except Exception:
+        return None
+
+
+# ----------------------------------------------------------------------------
+# clocks during the timed region
+# ----------------------------------------------------------------------------
+class ClockSampler:
+    FIELDS = ["clocks.sm", "clocks.max.sm", "clocks_event_reasons.hw_slowdown",
+              "clocks_event_reasons.hw_thermal_slowdown", "clocks_event_reasons.sw_thermal_slowdown",
+              "clocks_event_reasons.sw_power_cap", "power.draw"]
+
+    def __init__(self, device_index):
+        self.dev = device_index
+        self.samples = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.dev), "--query-gpu=" + ",".join(self.FIELDS),
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == len(self.FIELDS):
+                self.samples.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[j] for s in self.samples for j in range(4) if s[2 + j].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+# ----------------------------------------------------------------------------
+def cpu_baseline(w, target_path_steps=2.0e8):
+    """The oracle (as it stands) on a bounded sample of the same workload:
+    every time step i = N-1..0 on the cells k = 0, s, 2s, ... (s chosen so
+    the sample has ~target path-steps), all host cores (OpenMP)."""
+    import oracle
+    P = oracle.Problem(w)
+    total = workloads.path_steps(w)
+    stride = max(1, int(math.ceil(total / target_path_steps)))
+    ncell = (P.K + stride - 1) // stride
+    tab = P.new_table()
+    t0 = time.perf_counter()
+    for i in range(w["N"] - 1, -1, -1):
+        P.step(tab, i, 0, P.K, stride)
+    dt = time.perf_counter() - t0
+    sample_steps = ncell * w["M"] * w["N"] * (w["N"] + 1) // 2
+    return {"value": sample_steps / dt, "unit": "path-steps/s", "cores": oracle.num_threads(), "kind": "oracle",
+            "sample": "%s: all %d time steps on %d of %d cells (stride %d), M=%d: %.3g path-steps in %.1f s" % (
+                w["name"], w["N"], ncell, P.K, stride, w["M"], sample_steps, dt)}
+
+
+def run_reference(args, w, rank):
+    if rank != 0:
+        return 0
+    K, W = args.steps, args.warmup
+    vals = []
+    base = None
+    for s in range(W + K):
+        r = cpu_baseline(w, target_path_steps=args.ref_path_steps)
+        if s >= W:
+            vals.append(r["value"])
+            base = r
+    v = float(np.median(vals))
+    base["value"] = v
+    line = {"impl": "reference", "metric": "simulated path-steps/sec per SRMDP solve", "value": v,
+            "unit": "path-steps/s", "n_gpus": args.gpus, "steps": K, "warmup": W,
+            "ms_per_step": workloads.path_steps(w) / v * 1e3, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": config_block(w, args), "cpu_baseline": base,
+            "e2e": {"value": v, "unit": "path-steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "gpu_launches": 0}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def config_block(w, args):
+    return {"workload": w["name"], "d": w["d"], "q": w["q"], "N": w["N"], "cells_per_dim": w["C"],
+            "K": w["C"] ** w["d"], "M": w["M"], "problem": "PAPER.md §5.1 benchmark (X=W, mu=1, T=1, L=6.5)"
+            if w["f"] == "paper" else w["name"], "path_steps_per_solve": workloads.path_steps(w),
+            "parallelism": "cells sharded over %d GPU(s), ncclAllGather per time step" % args.gpus,
+            "l2": "flushed (256 MB write) before every timed solve"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="srmdp", choices=["srmdp", "reference"])
+    ap.add_argument("--config", default="cfg4", choices=sorted(workloads.CONFIGS))
+    ap.add_argument("--M", type=int, default=None)
+    ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ref-path-steps", type=float, default=2.0e8)
+    args = ap.parse_args()
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    kw = {"seed": args.seed}
+    if args.M:
+        kw["M"] = args.M
+    w = workloads.CONFIGS[args.config](**kw)
+    if args.impl == "reference":
+        return run_reference(args, w, rank)
+
+    import torch
+    import torch.distributed as dist
+    from paper_2407_21085_b200 import srmdp
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream(dev)
+    srmdp.library()
+
+    nccl_id = None
+    if world > 1:
+        obj = [srmdp.srmdp_nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nccl_id = obj[0]
+
+    def barrier():
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+
+    solver = srmdp.Solver(w, rank=rank, world=world, device=local, stream=stream.cuda_stream,
+                          flags=srmdp.FLAG_TIME_KERNELS, nccl_id=nccl_id)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+
+    for _ in range(args.warmup):
+        solver.solve()
+    barrier()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    kernel_ms = []
+    with ClockSampler(local) as clk:
+        barrier()
+        for s in range(args.steps):
+            flush.fill_(float(s))
+            ev[s][0].record(stream)
+            solver.solve()
+            ev[s][1].record(stream)
+            kernel_ms.append(solver.stats()["kernel_ms"])
+        barrier()
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    total_ms = float(sum(step_ms))
+    kern_ms = float(sum(kernel_ms))
+    if world > 1:
+        t = torch.tensor([total_ms, kern_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms, kern_ms = float(t[0]), float(t[1])
+    st = solver.stats()
+    path_steps = st["path_steps"]
+    value = path_steps * args.steps / (total_ms / 1e3)
+
+    # dominant kernel roofline: the fused step kernel (N launches per solve)
+    peak, peak_src = fp64_peak()
+    flops = algorithmic_flops(w) / world         # per rank per solve
+    launches_per_solve = st["kernel_launches"]
+    achieved = flops * args.steps / (kern_ms / 1e3) / 1e12
+    traffic = ncu_traffic()
+    roof = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+            "traffic": (traffic or {}).get("dram_bytes_per_launch"), "kernel": "srk::step_kernel<%d,%d>" % (w["d"], w["q"]),
+            "peak_source": peak_src, "flops_per_path_step": flops_per_path_step(w),
+            "flops_per_path_start": flops_per_path_start(w),
+            "kernel_share_of_step": kern_ms / total_ms, "avg_launch_ms": kern_ms / (args.steps * max(1, launches_per_solve))}
+    solver.close()
+
+    # e2e: the user's call sequence through the C ABI with host buffers:
+    # create (uploads parameters) -> solve -> coeffs of every slice to pinned host memory -> destroy
+    host = torch.empty((w["N"], st["K"], st["B"]), dtype=torch.float64).pin_memory()
+    hnp = host.numpy()
+    e2e_times = []
+    for s in range(1 + args.steps):
+        barrier()
+        t0 = time.perf_counter()
+        sv = srmdp.Solver(w, rank=rank, world=world, device=local, stream=stream.cuda_stream, nccl_id=nccl_id)
+        sv.solve()
+        for i in range(w["N"]):
+            sv.coeffs(i, 1, hnp[i])
+        sv.close()
+        barrier()
+        if s > 0:
+            e2e_times.append(time.perf_counter() - t0)
+    e2e_s = float(sum(e2e_times))
+    if world > 1:
+        t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t[0])
+    n_par = len(w.get("dyn_params", [])) + len(w.get("f_params", [])) + len(w.get("g_params", []))
+    h2d = 8 * (n_par + 3 * w["C"] + 2)
+    d2h = 8 * w["N"] * st["K"] * st["B"]
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(w)
+
+    if rank == 0:
+        line = {
+            "metric": "simulated path-steps/sec per SRMDP solve", "value": value, "unit": "path-steps/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded Philox clouds of the §5.1 benchmark; no dataset)",
+            "config": config_block(w, args),
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "e2e": {"value": path_steps * args.steps / e2e_s, "unit": "path-steps/s",
+                    "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                    "calls": "srmdp_create+srmdp_solve+srmdp_coeffs(all i, pinned host)+srmdp_destroy"},
+            "gpu_launches": launches_per_solve * args.steps,
+            "clocks": clk.summary(),
+            "lp0_fallbacks": st["lp0_fallbacks"],
+            "launch": {"grid": st["grid"], "block": st["block"], "smem_bytes": st["smem_bytes"],
+                       "ctas_per_sm": st["ctas_per_sm"]},
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

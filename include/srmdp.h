@@ -1,0 +1,153 @@
+/*
+ * srmdp.h — C ABI of the B200-native SRMDP hot path.
+ *
+ * Stratified Regression MDP (SRMDP) of Gobet, Lopez-Salas, Turkedjiev,
+ * Vazquez, arXiv 2407.21085 ("PAPER.md"; P:n = line n). The library computes
+ * the backward sweep of Alg. srmdp: for i = N-1 .. 0 and every
+ * hypercube H_k independently, M start points drawn from the conditional
+ * logistic law nu_k (Alg. stratify), Euler paths to T,
+ * MDP responses (eq. PsiM) reading the already-fitted affine (LP1,
+ * P:204-209) coefficients of later times, the per-cell Gram matrix and Z / Y
+ * right-hand sides, their least-squares solution (OLS), truncation
+ * at evaluation (eq. TL). Everything runs in fp64 CUDA kernels for
+ * sm_100a; there is no CPU fallback.
+ *
+ * Conventions (all entry points):
+ *  - Return an srmdp_status; 0 = OK, negative = error. No exception or exit()
+ *    crosses the ABI. srmdp_last_error() returns a human-readable message.
+ *  - Host pointers only (the library owns its device memory). Caller owns
+ *    every buffer it passes; configuration arrays are deep-copied by create.
+ *  - create / solve / destroy are collective over `world` ranks (one process
+ *    per GPU, SPMD); coeffs / eval are rank-local (the table is replicated).
+ *  - A handle is not thread-safe; distinct handles are independent.
+ *  - Random numbers: counter-based Philox4x32-10 keyed by `seed`
+ *    (docs/streams.md); results are a deterministic function of the config,
+ *    bit-identical for every `world`.
+ */
+#ifndef SRMDP_H
+#define SRMDP_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SRMDP_ABI_VERSION 1
+
+typedef struct srmdp srmdp_t; /* opaque: device table, streams, graph, NCCL comm */
+
+typedef enum {
+  SRMDP_OK = 0,
+  SRMDP_E_ARG = -1,         /* invalid argument (d=0, N<1, L<=0, mu<=0, T<=0, size mismatch, ...) */
+  SRMDP_E_PRECOND = -2,     /* M < d+1: OLS needs M >= dim L_Y (reading R14) */
+  SRMDP_E_STATE = -3,       /* coeffs/eval before a successful solve */
+  SRMDP_E_CUDA = -4,        /* CUDA runtime error (message has the CUDA string) */
+  SRMDP_E_NCCL = -5,        /* NCCL error / library not loadable for world > 1 */
+  SRMDP_E_NOMEM = -6,       /* device allocation failed */
+  SRMDP_E_UNSUPPORTED = -7  /* outside the compiled (d,q) set or the counter limits */
+} srmdp_status;
+
+/* Closed-form problem families (no host callbacks: they cannot run on the
+ * device). Parameter layouts, op order frozen by docs/streams.md §7:
+ *  dyn    BM     (q = d): X = W, paper §5.1               params: none
+ *         GBM    (q = d): b = mu o x, sigma = diag(s o x)           params: mu[d], s[d]
+ *         AFFINE        : b = b0 + B1 x, sigma = S0 (constant)      params: b0[d], B1[d*d], S0[d*q]
+ *  driver ZERO          : f = 0                                     params: none
+ *         LINEAR        : f = a y + theta.z + c                     params: a, c, theta[q]
+ *         PAPER         : f = (sum_k z_k)(y - (2+q)/(2q))   params: none
+ *  terminal AFFINE      : g = a + w.x                               params: a, w[d]
+ *         PAPER         : g = omega/(1+omega), omega = e^{T+sum x} params: none */
+typedef enum { SRMDP_DYN_BM = 0, SRMDP_DYN_GBM = 1, SRMDP_DYN_AFFINE = 2 } srmdp_dyn_kind;
+typedef enum { SRMDP_F_ZERO = 0, SRMDP_F_LINEAR = 1, SRMDP_F_PAPER = 2 } srmdp_f_kind;
+typedef enum { SRMDP_G_AFFINE = 0, SRMDP_G_PAPER = 1 } srmdp_g_kind;
+
+typedef struct {
+  int kind;             /* one of the enums above */
+  int n_params;         /* must equal the layout's length */
+  const double* params; /* host array, copied at create */
+} srmdp_fn;
+
+/* Flags */
+#define SRMDP_FLAG_NO_GRAPH     1 /* launch step kernels directly instead of replaying a CUDA graph */
+#define SRMDP_FLAG_TIME_KERNELS 2 /* record CUDA events around every step kernel (srmdp_stats.kernel_ms) */
+
+typedef struct {
+  int d, q, N;          /* state dim, Brownian dim, time steps */
+  double T;             /* horizon; dt = T/N */
+  srmdp_fn dyn, driver, terminal;
+  int cells_per_dim;    /* #C; K = #C^d hypercubes; breakpoints -L + j*2L/#C, outer cells infinite */
+  double L;             /* half-width of the uniformly stratified box [-L, L]^d */
+  double mu;            /* logistic parameter of nu (A_nu) — north_star's "nu" */
+  int64_t M;            /* simulations per hypercube and time step; M >= d+1 */
+  double C_g, C_f, L_f; /* bounds of (A_g), (A_f) -> C_y, C_z by eq. prop:bound */
+  double C_y_override;  /* NaN: use the bound; +INFINITY: no truncation; else this value */
+  double C_z_override;  /* same, for C_z */
+  uint64_t seed;        /* Philox key (docs/streams.md §2) */
+  int rank, world;      /* SPMD position; world == 1: no NCCL */
+  const void* nccl_unique_id; /* 128-byte ncclUniqueId from srmdp_nccl_unique_id (world > 1) */
+  int device;           /* CUDA device ordinal of this rank */
+  void* stream;         /* cudaStream_t to run on; NULL = a library-owned stream */
+  int flags;            /* SRMDP_FLAG_* */
+} srmdp_config;
+
+/* Validate, compute C_y/C_z, build the per-dimension breakpoint/F tables,
+ * allocate the N x K_pad x B_pad fp64 table (docs/layout.md), init NCCL.
+ * Collective. On error *out is NULL and srmdp_last_error(NULL) explains. */
+srmdp_status srmdp_create(const srmdp_config* cfg, srmdp_t** out);
+
+/* Run the whole backward sweep i = N-1 .. 0 (Alg. srmdp), one fused
+ * step kernel per time point on this rank's cells, then an in-place
+ * ncclAllGather of slice i (world > 1). Collective; blocks until done. */
+srmdp_status srmdp_solve(srmdp_t* h);
+
+/* Copy the coefficients of time i (0 <= i < N) to host `out`, K x B doubles,
+ * B = (q+1)(d+1), per cell [Y | Z_1 .. Z_q] each (d+1) long (docs/layout.md).
+ * basis 1: centered beta (native); basis 0: the paper's raw alpha.
+ * out_len must be exactly K*B. Coefficients are raw (truncation applies at
+ * evaluation). */
+srmdp_status srmdp_coeffs(const srmdp_t* h, int i, int basis, double* out, size_t out_len);
+
+/* Evaluate the truncated approximations at time i on n host points x (n x d,
+ * row-major): y[n] = T_{C_y}(y_i^(M)(x)), z[n x q] = T_{C_z}(z_i^(M)(x)) (may be
+ * NULL). i == N gives y = g(x) and requires z == NULL. */
+srmdp_status srmdp_eval(const srmdp_t* h, int i, size_t n, const double* x, double* y, double* z);
+
+void srmdp_destroy(srmdp_t* h);
+
+/* Per-handle message of the last failing call; NULL handle: this thread's
+ * last create error. Never NULL. */
+const char* srmdp_last_error(const srmdp_t* h);
+
+/* Rank 0 calls this and broadcasts the 128 bytes (e.g. torch.distributed). */
+srmdp_status srmdp_nccl_unique_id(void* out128);
+
+typedef struct {
+  double solve_ms;       /* host wall time of the last srmdp_solve */
+  double kernel_ms;      /* sum of step-kernel durations (needs SRMDP_FLAG_TIME_KERNELS) */
+  int kernel_launches;   /* step kernels in the last solve (= N) */
+  uint64_t path_steps;   /* K * M * N(N+1)/2 over all ranks */
+  uint64_t rank_path_steps; /* this rank's share */
+  uint64_t lp0_fallbacks;   /* rank-deficient (i,k) regressions (reading R15) */
+  int smallness_violated;   /* (T/N) L_f^2 > 1/(12 q): warning only */
+  double C_y, C_z;          /* truncation constants in use */
+  int64_t K, K_pad, chunk, k_begin, k_end; /* sharding (docs/layout.md) */
+  int B, B_pad;
+  int grid, block, smem_bytes, ctas_per_sm; /* launch configuration of the step kernel */
+} srmdp_stats_t;
+
+srmdp_status srmdp_stats(const srmdp_t* h, srmdp_stats_t* out);
+
+/* Pure host helper (no GPU): the contiguous cell range of `rank` among
+ * `world` ranks (docs/layout.md): out[0] = k_begin, out[1] = k_end,
+ * out[2] = chunk, out[3] = K_pad. */
+srmdp_status srmdp_shard_plan(int64_t K, int world, int rank, int64_t out[4]);
+
+/* Library version / build info string (ABI version, arch, compiled (d,q)). */
+const char* srmdp_build_info(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SRMDP_H */

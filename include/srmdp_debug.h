@@ -1,0 +1,35 @@
+/*
+ * srmdp_debug.h — test hooks of the SRMDP library (same .so as srmdp.h).
+ *
+ * They run the product's own __device__ functions (the ones the step kernel
+ * inlines) on the GPU and return their raw results, so tests can compare
+ * path states and transcendental bits with the CPU oracle element by element
+ * (docs/streams.md, docs/detmath.md). Host pointers; blocking; status codes
+ * as in srmdp.h. Not part of the hot path.
+ */
+#ifndef SRMDP_DEBUG_H
+#define SRMDP_DEBUG_H
+
+#include "srmdp.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Path trace of cloud (i,k), paths m = m0 .. m0+n-1 (docs/streams.md §2-7):
+ * x[n][N-i+1][d] = x_i .. x_N, cell[n][N-i+1] = located cells, dW[n][N-i][q].
+ * Uses the start-point sampler, Box-Muller, Euler and locate of the step kernel. */
+srmdp_status srmdp_debug_trace(const srmdp_t* h, int i, int64_t k, int64_t m0, int64_t n,
+                               double* x, int64_t* cell, double* dW);
+
+/* Elementwise device detmath (docs/detmath.md): op 0 = dm_log(in) -> out0;
+ * op 1 = dm_sincospi2(in) -> (out0 = sin, out1 = cos). */
+srmdp_status srmdp_debug_detmath(int op, size_t n, const double* in, double* out0, double* out1);
+
+/* Philox4x32-10 on the device: ctr[n][4], key[2] -> out[n][4]. */
+srmdp_status srmdp_debug_philox(size_t n, const uint32_t* ctr, const uint32_t key[2], uint32_t* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,117 @@
+// aux_kernels.cuh — evaluation kernel (srmdp_eval) and the test-hook kernels
+// of srmdp_debug.h. They inline the same __device__ functions as the step
+// kernel (problem.cuh, detmath.cuh, eval_block).
+#pragma once
+#include "step_kernel.cuh"
+
+namespace srk {
+
+// y_i^(M), z_i^(M) at n points (truncated); i == N: g.
+template <int D, int Q>
+__global__ void eval_kernel(const DevProblem P, const int i, const int64_t n, const double* __restrict__ xs,
+                            double* __restrict__ ys, double* __restrict__ zs) {
+  using KC = KCfg<D, Q>;
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  double x[D];
+#pragma unroll
+  for (int l = 0; l < D; ++l) x[l] = xs[t * D + l];
+  if (i == P.N) {
+    ys[t] = g_eval<D>(P, x);
+    return;
+  }
+  const double* cen = P.tabs + 2 * (P.C + 1);
+  uint32_t kn = 0;
+  double a[D + 1];
+  a[0] = 1.0;
+#pragma unroll
+  for (int l = 0; l < D; ++l) {
+    const int c = locate1(x[l], P.L, P.inv_delta, P.C);
+    kn = kn * (uint32_t)P.C + (uint32_t)c;
+    a[1 + l] = x[l] - __ldg(cen + c);
+  }
+  const double* blk = P.table + ((size_t)i * (size_t)P.K_pad + kn) * (size_t)KC::NBP;
+  double v = 0.0;
+#pragma unroll
+  for (int p = 0; p <= D; ++p) v = fma(__ldg(blk + p), a[p], v);
+  ys[t] = trunc_L(v, P.C_y);
+  if (zs) {
+    for (int l = 0; l < Q; ++l) {
+      double w = 0.0;
+#pragma unroll
+      for (int p = 0; p <= D; ++p) w = fma(__ldg(blk + (1 + l) * KC::N1 + p), a[p], w);
+      zs[t * Q + l] = trunc_L(w, P.C_z);
+    }
+  }
+}
+
+// Path trace (srmdp_debug_trace): start point, increments, Euler states and
+// located cells of paths m0 .. m0+n-1 of cloud (i,k).
+template <int D, int Q>
+__global__ void trace_kernel(const DevProblem P, const int i, const uint32_t k, const int64_t m0, const int64_t n,
+                             double* __restrict__ xs, int64_t* __restrict__ cells, double* __restrict__ dws) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  const uint32_t m = (uint32_t)(m0 + t);
+  const double* Fe = P.tabs;
+  const double* edge = P.tabs + (P.C + 1);
+  int cc[D];
+  {
+    uint32_t r = k;
+#pragma unroll
+    for (int l = D - 1; l >= 0; --l) { cc[l] = (int)(r % (uint32_t)P.C); r /= (uint32_t)P.C; }
+  }
+  const int steps = P.N - i;
+  double X[D];
+  start_point<D>(P, Fe, edge, cc, i, k, m, X);
+  double* xo = xs + t * (int64_t)(steps + 1) * D;
+  int64_t* co = cells + t * (int64_t)(steps + 1);
+  double* wo = dws + t * (int64_t)steps * Q;
+  auto put = [&](int s, const double (&v)[D]) {
+    uint32_t kn = 0;
+#pragma unroll
+    for (int l = 0; l < D; ++l) {
+      xo[s * D + l] = v[l];
+      kn = kn * (uint32_t)P.C + (uint32_t)locate1(v[l], P.L, P.inv_delta, P.C);
+    }
+    co[s] = kn;
+  };
+  put(0, X);
+  for (int j = i; j < P.N; ++j) {
+    double dW[Q], Xn[D];
+    brownian<Q>(P, i, j, k, m, dW);
+    euler<D, Q>(P, X, dW, Xn);
+#pragma unroll
+    for (int l = 0; l < Q; ++l) wo[(j - i) * Q + l] = dW[l];
+    put(j - i + 1, Xn);
+#pragma unroll
+    for (int l = 0; l < D; ++l) X[l] = Xn[l];
+  }
+}
+
+__global__ void detmath_kernel(const int op, const int64_t n, const double* __restrict__ in,
+                               double* __restrict__ o0, double* __restrict__ o1) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  if (op == 0) {
+    o0[t] = dm_log(in[t]);
+  } else {
+    double s, c;
+    dm_sincospi2(in[t], s, c);
+    o0[t] = s;
+    o1[t] = c;
+  }
+}
+
+__global__ void philox_kernel(const int64_t n, const uint32_t* __restrict__ ctr, const uint32_t k0,
+                              const uint32_t k1, uint32_t* __restrict__ out) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  const U4 o = philox4x32_10(U4{ctr[4 * t], ctr[4 * t + 1], ctr[4 * t + 2], ctr[4 * t + 3]}, k0, k1);
+  out[4 * t] = o.x;
+  out[4 * t + 1] = o.y;
+  out[4 * t + 2] = o.z;
+  out[4 * t + 3] = o.w;
+}
+
+}  // namespace srk

@@ -1,0 +1,659 @@
+// srmdp.cu — host orchestrator and C ABI (include/srmdp.h, include/srmdp_debug.h)
+// of the B200-native SRMDP backward sweep (arXiv 2407.21085, Alg. srmdp
+// P:332-365).
+//
+// One process per GPU. Each rank owns a contiguous cell range; per time point
+// i = N-1 .. 0 it launches the fused step kernel (step_kernel.cuh) on its
+// cells and all-gathers slice i in place over NCCL (NVLink/NVSwitch), so every
+// rank holds the full replicated coefficient table for the next step. The N
+// launches (+ collectives) are captured once into a CUDA graph and replayed.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <chrono>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/srmdp.h"
+#include "../../include/srmdp_debug.h"
+#include "aux_kernels.cuh"
+
+using namespace srk;
+
+// ------------------------------------------------------------------------
+// error plumbing
+// ------------------------------------------------------------------------
+static thread_local std::string g_create_err = "no error";
+
+#define SRMDP_FMT_ERR(dst, ...)                  \
+  do {                                           \
+    char _b[512];                                \
+    snprintf(_b, sizeof(_b), __VA_ARGS__);       \
+    (dst) = _b;                                  \
+  } while (0)
+
+// ------------------------------------------------------------------------
+// NCCL, loaded at run time (libnccl.so.2 is already mapped when torch is)
+// ------------------------------------------------------------------------
+struct NcclApi {
+  bool ok = false;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+  std::string err;
+};
+
+static NcclApi& nccl() {
+  static NcclApi api;
+  static bool tried = false;
+  if (tried) return api;
+  tried = true;
+  void* h = nullptr;
+  const char* env = getenv("SRMDP_NCCL_LIB");
+  if (env) h = dlopen(env, RTLD_NOW | RTLD_GLOBAL);
+  if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+  if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) {
+    api.err = std::string("cannot load libnccl.so.2: ") + dlerror();
+    return api;
+  }
+  api.GetUniqueId = (decltype(api.GetUniqueId))dlsym(h, "ncclGetUniqueId");
+  api.CommInitRank = (decltype(api.CommInitRank))dlsym(h, "ncclCommInitRank");
+  api.AllGather = (decltype(api.AllGather))dlsym(h, "ncclAllGather");
+  api.CommDestroy = (decltype(api.CommDestroy))dlsym(h, "ncclCommDestroy");
+  api.GetErrorString = (decltype(api.GetErrorString))dlsym(h, "ncclGetErrorString");
+  api.ok = api.GetUniqueId && api.CommInitRank && api.AllGather && api.CommDestroy && api.GetErrorString;
+  if (!api.ok) api.err = "libnccl.so.2 lacks a required symbol";
+  return api;
+}
+
+// ------------------------------------------------------------------------
+// host math of the grid (docs/streams.md §5, docs/detmath.md dm_exp,
+// docs/layout.md). Compiled with -ffp-contract=off: each op one rounding.
+// ------------------------------------------------------------------------
+static double host_dm_exp(double x) {
+  static const double E[15] = {
+      0x1p+0, 0x1p+0, 0x1p-1, 0x1.5555555555555p-3, 0x1.5555555555555p-5,
+      0x1.1111111111111p-7, 0x1.6c16c16c16c17p-10, 0x1.a01a01a01a01ap-13,
+      0x1.a01a01a01a01ap-16, 0x1.71de3a556c734p-19, 0x1.27e4fb7789f5cp-22,
+      0x1.ae64567f544e4p-26, 0x1.1eed8eff8d898p-29, 0x1.6124613a86d09p-33,
+      0x1.93974a8c07c9dp-37};
+  if (x != x) return x;
+  if (x > 709.782712893384) return INFINITY;
+  if (x < -745.1332191019412) return 0.0;
+  const double kf = std::rint(x * 0x1.71547652b82fep+0);
+  const double r = (x - (kf * 0x1.62e42fee00000p-1)) - (kf * 0x1.a39ef35793c76p-33);
+  double p = E[14];
+  for (int j = 13; j >= 0; --j) p = std::fma(p, r, E[j]);
+  return std::ldexp(p, (int)kf);
+}
+
+// F_nu(x) = 1/(1+exp(-mu x))
+static double host_F(double mu, double x) {
+  if (x == -INFINITY) return 0.0;
+  if (x == INFINITY) return 1.0;
+  return 1.0 / (1.0 + host_dm_exp(-(mu * x)));
+}
+
+// tabs = [F(e_c), c=0..C | e_c, c=0..C | r_c, c=0..C-1]
+static std::vector<double> grid_tables(int C, double L, double mu) {
+  std::vector<double> t(3 * C + 2);
+  const double delta = (2.0 * L) / (double)C;
+  for (int c = 0; c <= C; ++c) {
+    double e = (c == 0) ? -INFINITY : (c == C) ? INFINITY : ((-L) + ((double)c * delta));
+    t[C + 1 + c] = e;
+    t[c] = host_F(mu, e);
+  }
+  for (int c = 0; c < C; ++c) {
+    double r;
+    if (C == 1) r = 0.0;
+    else if (c == 0) r = (-L) + (1.0 * delta);
+    else if (c == C - 1) r = (-L) + ((double)(C - 1) * delta);
+    else r = (-L) + (((double)c + 0.5) * delta);
+    t[2 * (C + 1) + c] = r;
+  }
+  return t;
+}
+
+// ------------------------------------------------------------------------
+// per-(d,q) kernel dispatch
+// ------------------------------------------------------------------------
+struct Ops {
+  int D, Q;
+  cudaError_t (*prepare)(int C, int64_t M, bool by_smem, size_t* smem, int* ctas);
+  void (*step)(const DevProblem&, int, int64_t, int64_t, int, size_t, cudaStream_t);
+  void (*eval)(const DevProblem&, int, int64_t, const double*, double*, double*, cudaStream_t);
+  void (*trace)(const DevProblem&, int, uint32_t, int64_t, int64_t, double*, int64_t*, double*, cudaStream_t);
+};
+
+template <int D, int Q>
+static cudaError_t prepare_impl(int C, int64_t M, bool by_smem, size_t* smem, int* ctas) {
+  *smem = SmemLayout<D, Q>::bytes(C, M, by_smem);
+  cudaError_t e = cudaFuncSetAttribute(step_kernel<D, Q>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)*smem);
+  if (e != cudaSuccess) return e;
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(ctas, step_kernel<D, Q>, kThreads, *smem);
+}
+template <int D, int Q>
+static void step_impl(const DevProblem& P, int i, int64_t kb, int64_t nk, int grid, size_t smem, cudaStream_t s) {
+  step_kernel<D, Q><<<grid, kThreads, smem, s>>>(P, i, kb, nk);
+}
+template <int D, int Q>
+static void eval_impl(const DevProblem& P, int i, int64_t n, const double* x, double* y, double* z, cudaStream_t s) {
+  const int bs = 128;
+  eval_kernel<D, Q><<<(unsigned)((n + bs - 1) / bs), bs, 0, s>>>(P, i, n, x, y, z);
+}
+template <int D, int Q>
+static void trace_impl(const DevProblem& P, int i, uint32_t k, int64_t m0, int64_t n, double* x, int64_t* c,
+                       double* w, cudaStream_t s) {
+  const int bs = 64;
+  trace_kernel<D, Q><<<(unsigned)((n + bs - 1) / bs), bs, 0, s>>>(P, i, k, m0, n, x, c, w);
+}
+template <int D, int Q>
+static constexpr Ops make_ops() {
+  return Ops{D, Q, prepare_impl<D, Q>, step_impl<D, Q>, eval_impl<D, Q>, trace_impl<D, Q>};
+}
+
+// Compiled (d, q) set: d = q = 1..8 and the paper's high-d rows 11..19
+// (PAPER.md table:LP1d11 .. table:LP1d15_19), plus small d != q for AFFINE.
+static const Ops kOps[] = {
+    make_ops<1, 1>(),   make_ops<2, 2>(),   make_ops<3, 3>(),   make_ops<4, 4>(),
+    make_ops<5, 5>(),   make_ops<6, 6>(),   make_ops<7, 7>(),   make_ops<8, 8>(),
+    make_ops<11, 11>(), make_ops<12, 12>(), make_ops<13, 13>(), make_ops<14, 14>(),
+    make_ops<15, 15>(), make_ops<16, 16>(), make_ops<17, 17>(), make_ops<18, 18>(),
+    make_ops<19, 19>(), make_ops<1, 2>(),   make_ops<2, 1>(),   make_ops<2, 3>(),
+    make_ops<3, 2>(),
+};
+
+static const Ops* find_ops(int d, int q) {
+  for (const Ops& o : kOps)
+    if (o.D == d && o.Q == q) return &o;
+  return nullptr;
+}
+
+// ------------------------------------------------------------------------
+// the handle
+// ------------------------------------------------------------------------
+struct srmdp {
+  srmdp_config cfg{};
+  std::vector<double> params;  // [dyn | theta | g]
+  int d = 0, q = 0, N = 0, C = 0, B = 0, B_pad = 0;
+  int64_t K = 0, K_pad = 0, chunk = 0, k_begin = 0, k_end = 0, M = 0;
+  double C_y = 0, C_z = 0;
+  bool smallness_ok = true;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  double* d_table = nullptr;
+  double* d_params = nullptr;
+  double* d_tabs = nullptr;
+  double* d_scratch = nullptr;
+  unsigned long long* d_lp0 = nullptr;
+  double* d_io = nullptr;
+  size_t io_cap = 0;
+  DevProblem dp{};
+  const Ops* ops = nullptr;
+  int grid = 0, ctas = 0, sms = 0;
+  size_t smem = 0;
+  cudaGraphExec_t graph = nullptr;
+  ncclComm_t comm = nullptr;
+  bool solved = false;
+  std::vector<cudaEvent_t> ev;
+  srmdp_stats_t st{};
+  mutable std::string err = "no error";
+};
+
+static srmdp_status cuda_fail(const srmdp_t* h, cudaError_t e, const char* what) {
+  std::string m = std::string(what) + ": " + cudaGetErrorString(e);
+  if (h) h->err = m; else g_create_err = m;
+  return (e == cudaErrorMemoryAllocation) ? SRMDP_E_NOMEM : SRMDP_E_CUDA;
+}
+
+#define CK(h, call, what)                                  \
+  do {                                                     \
+    cudaError_t _e = (call);                               \
+    if (_e != cudaSuccess) return cuda_fail((h), _e, what); \
+  } while (0)
+
+extern "C" srmdp_status srmdp_shard_plan(int64_t K, int world, int rank, int64_t out[4]) {
+  if (K < 1 || world < 1 || rank < 0 || rank >= world || !out) return SRMDP_E_ARG;
+  const int64_t chunk = (K + world - 1) / world;
+  const int64_t K_pad = chunk * world;
+  int64_t b = (int64_t)rank * chunk, e = b + chunk;
+  if (b > K) b = K;
+  if (e > K) e = K;
+  out[0] = b;
+  out[1] = e;
+  out[2] = chunk;
+  out[3] = K_pad;
+  return SRMDP_OK;
+}
+
+static int expected_params(int which, int kind, int d, int q) {
+  if (which == 0) return kind == SRMDP_DYN_BM ? 0 : kind == SRMDP_DYN_GBM ? 2 * d : d + d * d + d * q;
+  if (which == 1) return kind == SRMDP_F_LINEAR ? 2 + q : 0;
+  return kind == SRMDP_G_AFFINE ? 1 + d : 0;
+}
+
+static srmdp_status validate(const srmdp_config* c, std::string& err) {
+  auto bad = [&](srmdp_status s, const char* m) { err = m; return s; };
+  if (!c) return bad(SRMDP_E_ARG, "cfg is NULL");
+  if (c->d < 1 || c->q < 1) return bad(SRMDP_E_ARG, "d and q must be >= 1");
+  if (c->N < 1) return bad(SRMDP_E_ARG, "N must be >= 1");
+  if (!(c->T > 0)) return bad(SRMDP_E_ARG, "T must be > 0");
+  if (c->cells_per_dim < 1) return bad(SRMDP_E_ARG, "cells_per_dim must be >= 1");
+  if (!(c->L > 0)) return bad(SRMDP_E_ARG, "L must be > 0");
+  if (!(c->mu > 0)) return bad(SRMDP_E_ARG, "mu must be > 0");
+  if (c->M < c->d + 1) return bad(SRMDP_E_PRECOND, "M < d+1: the LP1 OLS needs M >= d+1 (P:312)");
+  if (c->world < 1 || c->rank < 0 || c->rank >= c->world) return bad(SRMDP_E_ARG, "bad rank/world");
+  if (c->world > 1 && !c->nccl_unique_id) return bad(SRMDP_E_ARG, "world > 1 needs nccl_unique_id");
+  if (c->dyn.kind < 0 || c->dyn.kind > 2 || c->driver.kind < 0 || c->driver.kind > 2 || c->terminal.kind < 0 ||
+      c->terminal.kind > 1)
+    return bad(SRMDP_E_ARG, "unknown problem family kind");
+  if ((c->dyn.kind == SRMDP_DYN_BM || c->dyn.kind == SRMDP_DYN_GBM) && c->q != c->d)
+    return bad(SRMDP_E_ARG, "BM and GBM dynamics need q == d");
+  const srmdp_fn* fns[3] = {&c->dyn, &c->driver, &c->terminal};
+  for (int w = 0; w < 3; ++w) {
+    const int need = expected_params(w, fns[w]->kind, c->d, c->q);
+    if (fns[w]->n_params != need || (need > 0 && !fns[w]->params))
+      return bad(SRMDP_E_ARG, "parameter count does not match the family layout (srmdp.h)");
+  }
+  if (c->N >= (1 << 24)) return bad(SRMDP_E_UNSUPPORTED, "N >= 2^24 (Philox counter layout)");
+  if (c->M >= (int64_t)1 << 32) return bad(SRMDP_E_UNSUPPORTED, "M >= 2^32 (Philox counter layout)");
+  if (c->cells_per_dim > 2048) return bad(SRMDP_E_UNSUPPORTED, "cells_per_dim > 2048");
+  double K = 1;
+  for (int l = 0; l < c->d; ++l) K *= c->cells_per_dim;
+  if (K >= 4294967296.0) return bad(SRMDP_E_UNSUPPORTED, "K = C^d >= 2^32 (Philox counter layout)");
+  if (!find_ops(c->d, c->q)) return bad(SRMDP_E_UNSUPPORTED, "(d, q) not in the compiled set (srmdp_build_info)");
+  return SRMDP_OK;
+}
+
+// Prop. bound (eq. prop:bound).
+static void bounds(double C_g, double C_f, double L_f, int q, double T, int N, double* cy, double* cz, bool* ok) {
+  const double dt = T / (double)N;
+  const double Lf2 = L_f * L_f;
+  const double a = Lf2 > 1.0 ? Lf2 : 1.0;
+  const double Tv = T > 1.0 ? T : 1.0;
+  *cy = std::exp(T / 4.0 + 6.0 * q * a * Tv) * (C_g + T * C_f / (2.0 * std::sqrt((double)q)));
+  *cz = *cy / std::sqrt(dt);
+  *ok = dt * Lf2 <= 1.0 / (12.0 * q);
+}
+
+static srmdp_status enqueue_sweep(srmdp_t* h) {
+  const bool timed = h->cfg.flags & SRMDP_FLAG_TIME_KERNELS;
+  CK(h, cudaMemsetAsync(h->d_lp0, 0, sizeof(unsigned long long), h->stream), "memset");
+  const int64_t nk = h->k_end - h->k_begin;
+  for (int i = h->N - 1; i >= 0; --i) {
+    if (timed) CK(h, cudaEventRecordWithFlags(h->ev[2 * i], h->stream, cudaEventRecordExternal), "event");
+    if (nk > 0) h->ops->step(h->dp, i, h->k_begin, nk, h->grid, h->smem, h->stream);
+    CK(h, cudaGetLastError(), "step kernel launch");
+    if (timed) CK(h, cudaEventRecordWithFlags(h->ev[2 * i + 1], h->stream, cudaEventRecordExternal), "event");
+    if (h->cfg.world > 1) {
+      double* slice = h->d_table + (size_t)i * h->K_pad * h->B_pad;
+      const size_t cnt = (size_t)h->chunk * h->B_pad;
+      ncclResult_t r = nccl().AllGather(slice + (size_t)h->cfg.rank * cnt, slice, cnt, ncclDouble, h->comm, h->stream);
+      if (r != ncclSuccess) {
+        h->err = std::string("ncclAllGather: ") + nccl().GetErrorString(r);
+        return SRMDP_E_NCCL;
+      }
+    }
+  }
+  return SRMDP_OK;
+}
+
+extern "C" srmdp_status srmdp_create(const srmdp_config* cfg, srmdp_t** out) {
+  if (!out) { g_create_err = "out is NULL"; return SRMDP_E_ARG; }
+  *out = nullptr;
+  std::string verr;
+  srmdp_status vs = validate(cfg, verr);
+  if (vs != SRMDP_OK) { g_create_err = verr; return vs; }
+  srmdp_t* h = new srmdp();
+  h->cfg = *cfg;
+  h->d = cfg->d; h->q = cfg->q; h->N = cfg->N; h->C = cfg->cells_per_dim; h->M = cfg->M;
+  h->K = 1;
+  for (int l = 0; l < h->d; ++l) h->K *= h->C;
+  h->B = (h->q + 1) * (h->d + 1);
+  h->B_pad = h->B + (h->B & 1);
+  int64_t plan[4];
+  srmdp_shard_plan(h->K, cfg->world, cfg->rank, plan);
+  h->k_begin = plan[0]; h->k_end = plan[1]; h->chunk = plan[2]; h->K_pad = plan[3];
+  h->ops = find_ops(h->d, h->q);
+  // truncation constants: override, else eq. prop:bound (reading R5)
+  double by, bz;
+  bool ok;
+  bounds(cfg->C_g, cfg->C_f, cfg->L_f, h->q, cfg->T, h->N, &by, &bz, &ok);
+  h->smallness_ok = ok;
+  h->C_y = std::isnan(cfg->C_y_override) ? by : cfg->C_y_override;
+  h->C_z = std::isnan(cfg->C_z_override) ? bz : cfg->C_z_override;
+  // deep-copy parameters: [dyn | theta | g]
+  const int nd = cfg->dyn.n_params, nf = cfg->driver.n_params, ng = cfg->terminal.n_params;
+  h->params.assign(nd + (nf > 2 ? nf - 2 : 0) + ng + 1, 0.0);
+  for (int t = 0; t < nd; ++t) h->params[t] = cfg->dyn.params[t];
+  for (int t = 2; t < nf; ++t) h->params[nd + t - 2] = cfg->driver.params[t];
+  const int goff = nd + (nf > 2 ? nf - 2 : 0);
+  for (int t = 0; t < ng; ++t) h->params[goff + t] = cfg->terminal.params[t];
+  h->cfg.dyn.params = h->cfg.driver.params = h->cfg.terminal.params = nullptr;
+  h->cfg.nccl_unique_id = nullptr;
+
+  auto fail = [&](srmdp_status s) {
+    g_create_err = h->err;
+    srmdp_destroy(h);
+    return s;
+  };
+  cudaError_t e = cudaSetDevice(cfg->device);
+  if (e != cudaSuccess) { cuda_fail(h, e, "cudaSetDevice"); return fail(SRMDP_E_CUDA); }
+  if (cfg->stream) {
+    h->stream = (cudaStream_t)cfg->stream;
+  } else {
+    e = cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking);
+    if (e != cudaSuccess) { cuda_fail(h, e, "cudaStreamCreate"); return fail(SRMDP_E_CUDA); }
+    h->own_stream = true;
+  }
+  cudaDeviceProp prop;
+  cudaGetDeviceProperties(&prop, cfg->device);
+  h->sms = prop.multiProcessorCount;
+
+  const size_t table_bytes = (size_t)h->N * h->K_pad * h->B_pad * sizeof(double);
+  std::vector<double> tabs = grid_tables(h->C, cfg->L, cfg->mu);
+  if ((e = cudaMalloc(&h->d_table, table_bytes)) != cudaSuccess) { cuda_fail(h, e, "table alloc"); return fail(SRMDP_E_NOMEM); }
+  if ((e = cudaMalloc(&h->d_params, h->params.size() * sizeof(double))) != cudaSuccess ||
+      (e = cudaMalloc(&h->d_tabs, tabs.size() * sizeof(double))) != cudaSuccess ||
+      (e = cudaMalloc(&h->d_lp0, sizeof(unsigned long long))) != cudaSuccess) {
+    cuda_fail(h, e, "alloc");
+    return fail(SRMDP_E_NOMEM);
+  }
+  cudaMemcpy(h->d_params, h->params.data(), h->params.size() * sizeof(double), cudaMemcpyHostToDevice);
+  cudaMemcpy(h->d_tabs, tabs.data(), tabs.size() * sizeof(double), cudaMemcpyHostToDevice);
+
+  // launch configuration: persistent CTAs, (B_m, Y1_m) in smem when M <= 4096
+  const bool by_smem = h->M <= 4096;
+  e = h->ops->prepare(h->C, h->M, by_smem, &h->smem, &h->ctas);
+  if (e != cudaSuccess || h->ctas < 1) {
+    if (e == cudaSuccess) h->err = "step kernel does not fit on an SM";
+    else cuda_fail(h, e, "kernel attributes");
+    return fail(SRMDP_E_UNSUPPORTED);
+  }
+  const int64_t nk = h->k_end - h->k_begin;
+  const int64_t full = (int64_t)h->ctas * h->sms;
+  h->grid = (int)(nk < full ? (nk > 0 ? nk : 1) : full);
+  if (!by_smem) {
+    if ((e = cudaMalloc(&h->d_scratch, (size_t)h->grid * h->M * 2 * sizeof(double))) != cudaSuccess) {
+      cuda_fail(h, e, "scratch alloc");
+      return fail(SRMDP_E_NOMEM);
+    }
+  }
+
+  DevProblem& P = h->dp;
+  P.d = h->d; P.q = h->q; P.N = h->N; P.C = h->C; P.B = h->B; P.B_pad = h->B_pad;
+  P.dyn = cfg->dyn.kind; P.fk = cfg->driver.kind; P.gk = cfg->terminal.kind;
+  P.nbd = (h->d + 1) / 2; P.nbq = (h->q + 1) / 2;
+  P.by_in_smem = by_smem ? 1 : 0;
+  P.K = h->K; P.K_pad = h->K_pad; P.M = h->M;
+  P.T = cfg->T;
+  P.dt = cfg->T / (double)h->N;
+  P.sdt = std::sqrt(P.dt);
+  P.L = cfg->L;
+  P.inv_delta = (double)h->C / (2.0 * cfg->L);
+  P.neg_inv_mu = -(1.0 / cfg->mu);
+  P.C_y = h->C_y; P.C_z = h->C_z;
+  P.f_a = (cfg->driver.kind == SRMDP_F_LINEAR) ? cfg->driver.params[0] : 0.0;
+  P.f_c = (cfg->driver.kind == SRMDP_F_LINEAR) ? cfg->driver.params[1] : 0.0;
+  P.f_cq = (2.0 + (double)h->q) / (2.0 * (double)h->q);
+  P.key0 = (uint32_t)(cfg->seed & 0xffffffffu);
+  P.key1 = (uint32_t)(cfg->seed >> 32);
+  P.dyn_params = h->d_params;
+  P.theta = h->d_params + nd;
+  P.g_params = h->d_params + goff;
+  P.tabs = h->d_tabs;
+  P.table = h->d_table;
+  P.by_scratch = h->d_scratch;
+  P.lp0_count = h->d_lp0;
+
+  if (cfg->flags & SRMDP_FLAG_TIME_KERNELS) {
+    h->ev.resize(2 * h->N);
+    for (auto& x : h->ev) cudaEventCreate(&x);
+  }
+  if (cfg->world > 1) {
+    NcclApi& api = nccl();
+    if (!api.ok) { h->err = api.err; return fail(SRMDP_E_NCCL); }
+    ncclUniqueId id;
+    memcpy(&id, cfg->nccl_unique_id, sizeof(id));
+    ncclResult_t r = api.CommInitRank(&h->comm, cfg->world, id, cfg->rank);
+    if (r != ncclSuccess) { h->err = std::string("ncclCommInitRank: ") + api.GetErrorString(r); return fail(SRMDP_E_NCCL); }
+  }
+  h->st.path_steps = (uint64_t)h->K * (uint64_t)h->M * (uint64_t)h->N * (uint64_t)(h->N + 1) / 2;
+  h->st.rank_path_steps = (uint64_t)(h->k_end - h->k_begin) * (uint64_t)h->M * (uint64_t)h->N * (uint64_t)(h->N + 1) / 2;
+  *out = h;
+  return SRMDP_OK;
+}
+
+extern "C" srmdp_status srmdp_solve(srmdp_t* h) {
+  if (!h) return SRMDP_E_ARG;
+  auto t0 = std::chrono::steady_clock::now();
+  CK(h, cudaSetDevice(h->cfg.device), "cudaSetDevice");
+  const bool use_graph = !(h->cfg.flags & SRMDP_FLAG_NO_GRAPH);
+  if (use_graph) {
+    if (!h->graph) {
+      CK(h, cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal), "begin capture");
+      srmdp_status s = enqueue_sweep(h);
+      cudaGraph_t g = nullptr;
+      cudaError_t e = cudaStreamEndCapture(h->stream, &g);
+      if (s != SRMDP_OK) { if (g) cudaGraphDestroy(g); return s; }
+      if (e != cudaSuccess) return cuda_fail(h, e, "end capture");
+      e = cudaGraphInstantiate(&h->graph, g, 0);
+      cudaGraphDestroy(g);
+      if (e != cudaSuccess) return cuda_fail(h, e, "graph instantiate");
+    }
+    CK(h, cudaGraphLaunch(h->graph, h->stream), "graph launch");
+  } else {
+    srmdp_status s = enqueue_sweep(h);
+    if (s != SRMDP_OK) return s;
+  }
+  CK(h, cudaStreamSynchronize(h->stream), "solve");
+  unsigned long long lp0 = 0;
+  CK(h, cudaMemcpy(&lp0, h->d_lp0, sizeof(lp0), cudaMemcpyDeviceToHost), "lp0 count");
+  h->st.lp0_fallbacks = lp0;
+  h->st.kernel_launches = (h->k_end > h->k_begin) ? h->N : 0;
+  if (h->cfg.flags & SRMDP_FLAG_TIME_KERNELS) {
+    double tot = 0;
+    for (int i = 0; i < h->N; ++i) {
+      float ms = 0;
+      CK(h, cudaEventElapsedTime(&ms, h->ev[2 * i], h->ev[2 * i + 1]), "event time");
+      tot += ms;
+    }
+    h->st.kernel_ms = tot;
+  }
+  h->solved = true;
+  h->st.solve_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  return SRMDP_OK;
+}
+
+static void centers_host(const srmdp_t* h, int64_t k, double* r) {
+  const double L = h->cfg.L;
+  const int C = h->C;
+  const double delta = (2.0 * L) / (double)C;
+  int64_t rem = k;
+  for (int l = h->d - 1; l >= 0; --l) {
+    const int c = (int)(rem % C);
+    rem /= C;
+    if (C == 1) r[l] = 0.0;
+    else if (c == 0) r[l] = (-L) + (1.0 * delta);
+    else if (c == C - 1) r[l] = (-L) + ((double)(C - 1) * delta);
+    else r[l] = (-L) + (((double)c + 0.5) * delta);
+  }
+}
+
+extern "C" srmdp_status srmdp_coeffs(const srmdp_t* h, int i, int basis, double* out, size_t out_len) {
+  if (!h) return SRMDP_E_ARG;
+  if (!h->solved) { h->err = "coeffs before solve"; return SRMDP_E_STATE; }
+  if (i < 0 || i >= h->N || (basis != 0 && basis != 1) || !out || out_len != (size_t)h->K * h->B) {
+    h->err = "coeffs: bad i / basis / out_len (must be K*B)";
+    return SRMDP_E_ARG;
+  }
+  CK(h, cudaSetDevice(h->cfg.device), "cudaSetDevice");
+  const double* src = h->d_table + (size_t)i * h->K_pad * h->B_pad;
+  CK(h, cudaMemcpy2DAsync(out, h->B * sizeof(double), src, h->B_pad * sizeof(double), h->B * sizeof(double),
+                          (size_t)h->K, cudaMemcpyDeviceToHost, h->stream),
+     "coeffs copy");
+  CK(h, cudaStreamSynchronize(h->stream), "coeffs copy");
+  if (basis == 0) {  // raw alpha of P:718: alpha_0 = beta_0 - sum_j beta_j r_j
+    std::vector<double> r(h->d);
+    const int n1 = h->d + 1;
+    for (int64_t k = 0; k < h->K; ++k) {
+      centers_host(h, k, r.data());
+      for (int o = 0; o <= h->q; ++o) {
+        double* b = out + (size_t)k * h->B + (size_t)o * n1;
+        double s = b[0];
+        for (int j = 0; j < h->d; ++j) s -= b[1 + j] * r[j];
+        b[0] = s;
+      }
+    }
+  }
+  return SRMDP_OK;
+}
+
+static srmdp_status ensure_io(const srmdp_t* hc, size_t bytes) {
+  srmdp_t* h = const_cast<srmdp_t*>(hc);
+  if (h->io_cap >= bytes) return SRMDP_OK;
+  if (h->d_io) cudaFree(h->d_io);
+  h->d_io = nullptr;
+  h->io_cap = 0;
+  CK(h, cudaMalloc(&h->d_io, bytes), "io alloc");
+  h->io_cap = bytes;
+  return SRMDP_OK;
+}
+
+extern "C" srmdp_status srmdp_eval(const srmdp_t* h, int i, size_t n, const double* x, double* y, double* z) {
+  if (!h) return SRMDP_E_ARG;
+  if (i < 0 || i > h->N || (n > 0 && (!x || !y)) || (i == h->N && z)) {
+    h->err = "eval: bad i, NULL buffer, or z requested at i == N";
+    return SRMDP_E_ARG;
+  }
+  if (i < h->N && !h->solved) { h->err = "eval before solve"; return SRMDP_E_STATE; }
+  if (n == 0) return SRMDP_OK;
+  CK(h, cudaSetDevice(h->cfg.device), "cudaSetDevice");
+  const size_t nx = n * h->d, nz = z ? n * h->q : 0;
+  srmdp_status s = ensure_io(h, (nx + n + nz) * sizeof(double));
+  if (s != SRMDP_OK) return s;
+  double* dx = h->d_io;
+  double* dy = dx + nx;
+  double* dz = z ? dy + n : nullptr;
+  CK(h, cudaMemcpyAsync(dx, x, nx * sizeof(double), cudaMemcpyHostToDevice, h->stream), "eval h2d");
+  h->ops->eval(h->dp, i, (int64_t)n, dx, dy, dz, h->stream);
+  CK(h, cudaGetLastError(), "eval kernel");
+  CK(h, cudaMemcpyAsync(y, dy, n * sizeof(double), cudaMemcpyDeviceToHost, h->stream), "eval d2h");
+  if (z) CK(h, cudaMemcpyAsync(z, dz, nz * sizeof(double), cudaMemcpyDeviceToHost, h->stream), "eval d2h");
+  CK(h, cudaStreamSynchronize(h->stream), "eval");
+  return SRMDP_OK;
+}
+
+extern "C" void srmdp_destroy(srmdp_t* h) {
+  if (!h) return;
+  cudaSetDevice(h->cfg.device);
+  if (h->stream) cudaStreamSynchronize(h->stream);
+  if (h->graph) cudaGraphExecDestroy(h->graph);
+  for (auto& e : h->ev) cudaEventDestroy(e);
+  if (h->comm && nccl().ok) nccl().CommDestroy(h->comm);
+  cudaFree(h->d_table);
+  cudaFree(h->d_params);
+  cudaFree(h->d_tabs);
+  cudaFree(h->d_scratch);
+  cudaFree(h->d_lp0);
+  cudaFree(h->d_io);
+  if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
+  delete h;
+}
+
+extern "C" const char* srmdp_last_error(const srmdp_t* h) { return h ? h->err.c_str() : g_create_err.c_str(); }
+
+extern "C" srmdp_status srmdp_nccl_unique_id(void* out128) {
+  if (!out128) return SRMDP_E_ARG;
+  NcclApi& api = nccl();
+  if (!api.ok) { g_create_err = api.err; return SRMDP_E_NCCL; }
+  ncclUniqueId id;
+  ncclResult_t r = api.GetUniqueId(&id);
+  if (r != ncclSuccess) { g_create_err = std::string("ncclGetUniqueId: ") + api.GetErrorString(r); return SRMDP_E_NCCL; }
+  memcpy(out128, &id, sizeof(id));
+  return SRMDP_OK;
+}
+
+extern "C" srmdp_status srmdp_stats(const srmdp_t* h, srmdp_stats_t* out) {
+  if (!h || !out) return SRMDP_E_ARG;
+  srmdp_stats_t s = h->st;
+  s.smallness_violated = h->smallness_ok ? 0 : 1;
+  s.C_y = h->C_y;
+  s.C_z = h->C_z;
+  s.K = h->K; s.K_pad = h->K_pad; s.chunk = h->chunk; s.k_begin = h->k_begin; s.k_end = h->k_end;
+  s.B = h->B; s.B_pad = h->B_pad;
+  s.grid = h->grid; s.block = kThreads; s.smem_bytes = (int)h->smem; s.ctas_per_sm = h->ctas;
+  *out = s;
+  return SRMDP_OK;
+}
+
+extern "C" const char* srmdp_build_info(void) {
+  static std::string info;
+  if (info.empty()) {
+    info = "srmdp ABI " + std::to_string(SRMDP_ABI_VERSION) + "; sm_100a fp64; (d,q) =";
+    for (const Ops& o : kOps) info += " (" + std::to_string(o.D) + "," + std::to_string(o.Q) + ")";
+  }
+  return info.c_str();
+}
+
+// ------------------------------------------------------------------------
+// test hooks (include/srmdp_debug.h)
+// ------------------------------------------------------------------------
+extern "C" srmdp_status srmdp_debug_trace(const srmdp_t* h, int i, int64_t k, int64_t m0, int64_t n, double* x,
+                                          int64_t* cell, double* dW) {
+  if (!h || i < 0 || i >= h->N || k < 0 || k >= h->K || m0 < 0 || n < 1 || !x || !cell || !dW) return SRMDP_E_ARG;
+  CK(h, cudaSetDevice(h->cfg.device), "cudaSetDevice");
+  const int steps = h->N - i;
+  const size_t nx = (size_t)n * (steps + 1) * h->d, nc = (size_t)n * (steps + 1), nw = (size_t)n * steps * h->q;
+  srmdp_status s = ensure_io(h, (nx + nc + nw) * sizeof(double));
+  if (s != SRMDP_OK) return s;
+  double* dx = h->d_io;
+  int64_t* dc = reinterpret_cast<int64_t*>(dx + nx);
+  double* dw = dx + nx + nc;
+  h->ops->trace(h->dp, i, (uint32_t)k, m0, n, dx, dc, dw, h->stream);
+  CK(h, cudaGetLastError(), "trace kernel");
+  CK(h, cudaMemcpyAsync(x, dx, nx * sizeof(double), cudaMemcpyDeviceToHost, h->stream), "trace d2h");
+  CK(h, cudaMemcpyAsync(cell, dc, nc * sizeof(int64_t), cudaMemcpyDeviceToHost, h->stream), "trace d2h");
+  CK(h, cudaMemcpyAsync(dW, dw, nw * sizeof(double), cudaMemcpyDeviceToHost, h->stream), "trace d2h");
+  CK(h, cudaStreamSynchronize(h->stream), "trace");
+  return SRMDP_OK;
+}
+
+extern "C" srmdp_status srmdp_debug_detmath(int op, size_t n, const double* in, double* out0, double* out1) {
+  if ((op != 0 && op != 1) || !in || !out0 || (op == 1 && !out1)) return SRMDP_E_ARG;
+  if (n == 0) return SRMDP_OK;
+  double* d = nullptr;
+  cudaError_t e = cudaMalloc(&d, 3 * n * sizeof(double));
+  if (e != cudaSuccess) return cuda_fail(nullptr, e, "detmath alloc");
+  cudaMemcpy(d, in, n * sizeof(double), cudaMemcpyHostToDevice);
+  detmath_kernel<<<(unsigned)((n + 255) / 256), 256>>>(op, (int64_t)n, d, d + n, d + 2 * n);
+  e = cudaDeviceSynchronize();
+  if (e == cudaSuccess) {
+    cudaMemcpy(out0, d + n, n * sizeof(double), cudaMemcpyDeviceToHost);
+    if (op == 1) cudaMemcpy(out1, d + 2 * n, n * sizeof(double), cudaMemcpyDeviceToHost);
+  }
+  cudaFree(d);
+  return e == cudaSuccess ? SRMDP_OK : cuda_fail(nullptr, e, "detmath kernel");
+}
+
+extern "C" srmdp_status srmdp_debug_philox(size_t n, const uint32_t* ctr, const uint32_t key[2], uint32_t* out) {
+  if (!ctr || !key || !out) return SRMDP_E_ARG;
+  if (n == 0) return SRMDP_OK;
+  uint32_t* d = nullptr;
+  cudaError_t e = cudaMalloc(&d, 8 * n * sizeof(uint32_t));
+  if (e != cudaSuccess) return cuda_fail(nullptr, e, "philox alloc");
+  cudaMemcpy(d, ctr, 4 * n * sizeof(uint32_t), cudaMemcpyHostToDevice);
+  philox_kernel<<<(unsigned)((n + 255) / 256), 256>>>((int64_t)n, d, key[0], key[1], d + 4 * n);
+  e = cudaDeviceSynchronize();
+  if (e == cudaSuccess) cudaMemcpy(out, d + 4 * n, 4 * n * sizeof(uint32_t), cudaMemcpyDeviceToHost);
+  cudaFree(d);
+  return e == cudaSuccess ? SRMDP_OK : cuda_fail(nullptr, e, "philox kernel");
+}

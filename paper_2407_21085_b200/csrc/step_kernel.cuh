@@ -1,0 +1,380 @@
+// step_kernel.cuh — the fused SRMDP time-step kernel (one launch per t_i).
+//
+// For every owned hypercube H_k (one persistent CTA walks cells k = blockIdx,
+// blockIdx + gridDim, ...), Alg. srmdp at time i:
+//  pass 1  each thread simulates one path per round (M/256 rounds):
+//          conditional-logistic start point, Euler chain to T
+//           with locate + gather of the fitted block of the cell
+//          the path lands in, truncated evaluation (eq. TL) and
+//          the multistep response S_{Y,i+1} (eq. PsiM). The design
+//          row (1, x_i - r_k) and the Z responses S_{Y,i+1} dW_i / dt go to a
+//          shared-memory row buffer; owner-compute threads fold them into the
+//          Gram matrix and Z right-hand sides in a fixed order.
+//  solve   Cholesky of the (d+1)^2 Gram (thread 0), q triangular solves
+//          -> beta^Z (same OLS minimiser as the paper's QR).
+//  pass 2  S_{Y,i} = S_{Y,i+1} + f_i(x_i, y_{i+1}(x_{i+1}), z_i(x_i)) dt with
+//          the fresh z_i of this cell, warp-shuffle + fixed-order
+//          block reduction of the Y right-hand side, solve -> beta^Y.
+//  store   [beta^Y | beta^Z_1..q] into table[i][k] (docs/layout.md).
+// Reduction orders depend only on (M, thread count), never on the number of
+// ranks, so tables are bit-identical for every world size.
+#pragma once
+#include "problem.cuh"
+
+namespace srk {
+
+constexpr int kThreads = 256;
+
+template <int D, int Q>
+struct KCfg {
+  static constexpr int N1 = D + 1;
+  static constexpr int NB = (Q + 1) * N1;           // B
+  static constexpr int NBP = NB + (NB & 1);         // B_pad
+  static constexpr int NG = N1 * (N1 + 1) / 2;      // Gram entries (upper, incl. diag)
+  static constexpr int NZ = Q * N1;                 // Z right-hand-side entries
+  static constexpr int E = NG + NZ;
+  static constexpr int S = (E <= kThreads) ? (kThreads / E) : 1;  // row slices per entry
+  static constexpr int PAIRS = E * S;
+  static constexpr int NACC = (PAIRS + kThreads - 1) / kThreads;
+  static constexpr int ROW = (1 + D + Q) | 1;       // [1 | x - r_k | S dW/dt], odd stride
+  static constexpr bool KEEP_DWI = (Q <= 8);
+  static constexpr bool UNROLL_GATHER = (NB <= 128);
+};
+
+// Shared-memory carve-up (in doubles), shared by host sizing and the kernel.
+template <int D, int Q>
+struct SmemLayout {
+  using KC = KCfg<D, Q>;
+  __host__ __device__ static int tabs(int C) { return (3 * C + 2 + 1) & ~1; }
+  __host__ __device__ static int rows(int C) { return tabs(C); }
+  __host__ __device__ static int L(int C) { return rows(C) + kThreads * KC::ROW; }
+  __host__ __device__ static int RZ(int C) { return L(C) + KC::N1 * KC::N1; }
+  __host__ __device__ static int BZ(int C) { return RZ(C) + KC::NZ; }
+  __host__ __device__ static int BY(int C) { return BZ(C) + KC::NZ; }
+  __host__ __device__ static int RY(int C) { return BY(C) + KC::N1; }
+  __host__ __device__ static int warp(int C) { return RY(C) + KC::N1; }
+  __host__ __device__ static int flag(int C) { return warp(C) + (kThreads / 32) * KC::N1; }
+  __host__ __device__ static int pairs(int C) { return flag(C) + 2; }
+  __host__ __device__ static size_t bytes(int C, int64_t M, bool by_in_smem) {
+    return sizeof(double) * ((size_t)pairs(C) + (by_in_smem ? 2 * (size_t)M : 0));
+  }
+};
+
+// Evaluate the fitted block of a cell at centered coordinates a = (1, x - r):
+// y = T_{C_y}(beta^Y . a), zlin = sum_l w_l T_{C_z}(beta^{Z_l} . a).
+template <int D, int Q>
+__device__ __forceinline__ void eval_block(const DevProblem& P, const double* __restrict__ blk,
+                                           const double (&a)[D + 1], double& y, double& zlin) {
+  using KC = KCfg<D, Q>;
+  if constexpr (KC::UNROLL_GATHER) {
+    double out[Q + 1];
+#pragma unroll
+    for (int o = 0; o <= Q; ++o) out[o] = 0.0;
+    const double2* b2 = reinterpret_cast<const double2*>(blk);
+#pragma unroll
+    for (int u = 0; u < KC::NBP / 2; ++u) {
+      const double2 v = __ldg(b2 + u);
+      const int e0 = 2 * u, e1 = 2 * u + 1;
+      out[e0 / KC::N1] = fma(v.x, a[e0 % KC::N1], out[e0 / KC::N1]);
+      if (e1 < KC::NB) out[e1 / KC::N1] = fma(v.y, a[e1 % KC::N1], out[e1 / KC::N1]);
+    }
+    y = trunc_L(out[0], P.C_y);
+    double zl = 0.0;
+#pragma unroll
+    for (int l = 0; l < Q; ++l) zl = fma(zweight(P, l), trunc_L(out[1 + l], P.C_z), zl);
+    zlin = zl;
+  } else {
+    double acc = 0.0;
+#pragma unroll
+    for (int p = 0; p <= D; ++p) acc = fma(__ldg(blk + p), a[p], acc);
+    y = trunc_L(acc, P.C_y);
+    double zl = 0.0;
+#pragma unroll 1
+    for (int l = 0; l < Q; ++l) {
+      const double* bz = blk + (1 + l) * KC::N1;
+      double v = 0.0;
+#pragma unroll
+      for (int p = 0; p <= D; ++p) v = fma(__ldg(bz + p), a[p], v);
+      zl = fma(zweight(P, l), trunc_L(v, P.C_z), zl);
+    }
+    zlin = zl;
+  }
+}
+
+// One path of cloud (i,k): start point x_i, then the Euler chain with the
+// multistep response. Returns B = S_{Y,i+1}(x_i) = g(x_N) + sum_{j>i} f_j dt
+// (eq. PsiM), Y1 = y_{i+1}(x_{i+1}) and dW_i.
+template <int D, int Q>
+__device__ __forceinline__ void simulate_path(const DevProblem& P, const double* sFe, const double* sEdge,
+                                              const double* sCen, const int (&cc)[D], int i, uint32_t k,
+                                              uint32_t m, double (&x)[D], double& Bout, double& Y1out,
+                                              double (&dWi)[Q]) {
+  using KC = KCfg<D, Q>;
+  start_point<D>(P, sFe, sEdge, cc, i, k, m, x);
+  double X[D];
+#pragma unroll
+  for (int l = 0; l < D; ++l) X[l] = x[l];
+  double acc = 0.0, zlin = 0.0, Y1 = 0.0, yv = 0.0;
+  const int N = P.N;
+  for (int j = i; j < N; ++j) {
+    double dW[Q];
+    brownian<Q>(P, i, j, k, m, dW);
+    if (KC::KEEP_DWI && j == i) {
+#pragma unroll
+      for (int l = 0; l < Q; ++l) dWi[l] = dW[l];
+    }
+    double Xn[D];
+    euler<D, Q>(P, X, dW, Xn);
+    double zn = 0.0;
+    if (j + 1 < N) {
+      // locate X_{j+1} ((A_Strat.), docs/streams.md §6) and gather its block
+      uint32_t kn = 0;
+      double a[D + 1];
+      a[0] = 1.0;
+#pragma unroll
+      for (int l = 0; l < D; ++l) {
+        const int c = locate1(Xn[l], P.L, P.inv_delta, P.C);
+        kn = kn * (uint32_t)P.C + (uint32_t)c;
+        a[1 + l] = Xn[l] - sCen[c];
+      }
+      const double* blk = P.table + ((size_t)(j + 1) * (size_t)P.K_pad + kn) * (size_t)KC::NBP;
+      eval_block<D, Q>(P, blk, a, yv, zn);
+    } else {
+      yv = g_eval<D>(P, Xn);                      // y_N := g
+    }
+    if (j == i) {
+      Y1 = yv;
+    } else {
+      const double fdt = f_eval(P, yv, zlin) * P.dt;   // f_j(x_j, y_{j+1}(x_{j+1}), z_j(x_j)) dt
+      acc = acc + fdt;
+    }
+    zlin = zn;
+#pragma unroll
+    for (int l = 0; l < D; ++l) X[l] = Xn[l];
+  }
+  Bout = yv + acc;                                 // g(x_N) + sum
+  Y1out = Y1;
+  if (!KC::KEEP_DWI) brownian<Q>(P, i, i, k, m, dWi);
+}
+
+// Cholesky of the symmetric n x n matrix in A (full storage), lower factor in
+// place. Returns 1 iff positive definite with min diag(L) >= 1e-10 max diag(L)
+// (= QR's |R_jj| test, reading R15).
+template <int N1>
+__device__ int cholesky_inplace(double* A) {
+  double mx = 0.0, mn = 1e300;
+  for (int j = 0; j < N1; ++j) {
+    double s = A[j * N1 + j];
+    for (int kk = 0; kk < j; ++kk) s = s - A[j * N1 + kk] * A[j * N1 + kk];
+    if (!(s > 0.0)) return 0;
+    const double ljj = sqrt(s);
+    A[j * N1 + j] = ljj;
+    mx = fmax(mx, ljj);
+    mn = fmin(mn, ljj);
+    for (int r = j + 1; r < N1; ++r) {
+      double t = A[r * N1 + j];
+      for (int kk = 0; kk < j; ++kk) t = t - A[r * N1 + kk] * A[j * N1 + kk];
+      A[r * N1 + j] = t / ljj;
+    }
+  }
+  return (mn >= 1e-10 * mx) ? 1 : 0;
+}
+
+// Solve L L^T b = r (L lower in full storage).
+template <int N1>
+__device__ void chol_solve(const double* L, const double* r, double* b) {
+  double y[N1];
+  for (int p = 0; p < N1; ++p) {
+    double s = r[p];
+    for (int kk = 0; kk < p; ++kk) s = s - L[p * N1 + kk] * y[kk];
+    y[p] = s / L[p * N1 + p];
+  }
+  for (int p = N1 - 1; p >= 0; --p) {
+    double s = y[p];
+    for (int kk = p + 1; kk < N1; ++kk) s = s - L[kk * N1 + p] * b[kk];
+    b[p] = s / L[p * N1 + p];
+  }
+}
+
+template <int D, int Q>
+__global__ void __launch_bounds__(kThreads, 2)
+step_kernel(const DevProblem P, const int i, const int64_t k_begin, const int64_t nk) {
+  using KC = KCfg<D, Q>;
+  using SL = SmemLayout<D, Q>;
+  extern __shared__ double sm[];
+  const int C = P.C;
+  const int tid = threadIdx.x;
+  double* sFe = sm;
+  double* sEdge = sm + (C + 1);
+  double* sCen = sm + 2 * (C + 1);
+  double* sRows = sm + SL::rows(C);
+  double* sL = sm + SL::L(C);
+  double* sRZ = sm + SL::RZ(C);
+  double* sBZ = sm + SL::BZ(C);
+  double* sBY = sm + SL::BY(C);
+  double* sRY = sm + SL::RY(C);
+  double* sWarp = sm + SL::warp(C);
+  int* sFlag = reinterpret_cast<int*>(sm + SL::flag(C));
+  double* BYs = P.by_in_smem ? (sm + SL::pairs(C)) : (P.by_scratch + (size_t)blockIdx.x * (size_t)P.M * 2);
+
+  for (int t = tid; t < 3 * C + 2; t += kThreads) sm[t] = P.tabs[t];
+
+  // Owner-compute assignment: pair idx -> (entry e, row slice s); fixed per thread.
+  int cA[KC::NACC], cB[KC::NACC], rlo[KC::NACC], rhi[KC::NACC];
+#pragma unroll
+  for (int n = 0; n < KC::NACC; ++n) {
+    const int idx = tid + n * kThreads;
+    if (idx < KC::PAIRS) {
+      const int e = idx % KC::E, s = idx / KC::E;
+      if (e < KC::NG) {               // Gram (p <= q), row-major upper enumeration
+        int p = 0, rem = e;
+        while (rem >= KC::N1 - p) { rem -= KC::N1 - p; ++p; }
+        cA[n] = p;
+        cB[n] = p + rem;
+      } else {                        // Z RHS: (l, p) -> a'_p * R_l
+        const int z = e - KC::NG;
+        cA[n] = z % KC::N1;
+        cB[n] = 1 + D + z / KC::N1;
+      }
+      rlo[n] = (s * kThreads) / KC::S;
+      rhi[n] = ((s + 1) * kThreads) / KC::S;
+    } else {
+      cA[n] = cB[n] = 0;
+      rlo[n] = rhi[n] = 0;
+    }
+  }
+  __syncthreads();
+
+  const int64_t M = P.M;
+  const double dt = P.dt;
+  for (int64_t kl = blockIdx.x; kl < nk; kl += gridDim.x) {
+    const uint32_t k = (uint32_t)(k_begin + kl);
+    int cc[D];
+    {
+      uint32_t r = k;
+#pragma unroll
+      for (int l = D - 1; l >= 0; --l) { cc[l] = (int)(r % (uint32_t)C); r /= (uint32_t)C; }
+    }
+    double rk[D];
+#pragma unroll
+    for (int l = 0; l < D; ++l) rk[l] = sCen[cc[l]];
+
+    // ---------------- pass 1: paths, Gram and Z right-hand sides ----------
+    double acc[KC::NACC];
+#pragma unroll
+    for (int n = 0; n < KC::NACC; ++n) acc[n] = 0.0;
+    for (int64_t m0 = 0; m0 < M; m0 += kThreads) {
+      const int64_t m = m0 + tid;
+      const int nrows = (int)((M - m0) < kThreads ? (M - m0) : kThreads);
+      if (m < M) {
+        double x[D], dWi[Q], Bv, Y1;
+        simulate_path<D, Q>(P, sFe, sEdge, sCen, cc, i, k, (uint32_t)m, x, Bv, Y1, dWi);
+        double* row = sRows + tid * KC::ROW;
+        row[0] = 1.0;
+#pragma unroll
+        for (int l = 0; l < D; ++l) row[1 + l] = x[l] - rk[l];
+#pragma unroll
+        for (int l = 0; l < Q; ++l) row[1 + D + l] = (Bv * dWi[l]) / dt;   // S_{Z,i} = S_{Y,i+1} w / dt
+        BYs[2 * m] = Bv;
+        BYs[2 * m + 1] = Y1;
+      }
+      __syncthreads();
+#pragma unroll
+      for (int n = 0; n < KC::NACC; ++n) {
+        const int hi = rhi[n] < nrows ? rhi[n] : nrows;
+        double a = acc[n];
+        for (int r = rlo[n]; r < hi; ++r) a = fma(sRows[r * KC::ROW + cA[n]], sRows[r * KC::ROW + cB[n]], a);
+        acc[n] = a;
+      }
+      __syncthreads();
+    }
+    // fixed-order combination of the row-slice partials
+    double* red = sRows;
+#pragma unroll
+    for (int n = 0; n < KC::NACC; ++n) {
+      const int idx = tid + n * kThreads;
+      if (idx < KC::PAIRS) red[(idx % KC::E) * KC::S + idx / KC::E] = acc[n];
+    }
+    __syncthreads();
+    for (int e = tid; e < KC::E; e += kThreads) {
+      double v = red[e * KC::S];
+      for (int s = 1; s < KC::S; ++s) v = v + red[e * KC::S + s];
+      if (e < KC::NG) {
+        int p = 0, rem = e;
+        while (rem >= KC::N1 - p) { rem -= KC::N1 - p; ++p; }
+        const int q2 = p + rem;
+        sL[p * KC::N1 + q2] = v;
+        sL[q2 * KC::N1 + p] = v;
+      } else {
+        const int z = e - KC::NG;
+        sRZ[(z / KC::N1) * KC::N1 + z % KC::N1] = v;   // [l][p]
+      }
+    }
+    __syncthreads();
+    if (tid == 0) sFlag[0] = cholesky_inplace<KC::N1>(sL);
+    __syncthreads();
+    const int ok = sFlag[0];
+    // ---------------- solve Z ---------------------------------
+    for (int l = tid; l < Q; l += kThreads) {
+      if (ok) {
+        chol_solve<KC::N1>(sL, sRZ + l * KC::N1, sBZ + l * KC::N1);
+      } else {                                     // LP0 fallback: mean
+        sBZ[l * KC::N1] = sRZ[l * KC::N1] / (double)M;
+        for (int p = 1; p < KC::N1; ++p) sBZ[l * KC::N1 + p] = 0.0;
+      }
+    }
+    __syncthreads();
+
+    // ---------------- pass 2: Y responses with the fresh z_i ---
+    double ry[KC::N1];
+#pragma unroll
+    for (int p = 0; p < KC::N1; ++p) ry[p] = 0.0;
+    for (int64_t m = tid; m < M; m += kThreads) {
+      double x[D], a[KC::N1];
+      start_point<D>(P, sFe, sEdge, cc, i, k, (uint32_t)m, x);
+      a[0] = 1.0;
+#pragma unroll
+      for (int l = 0; l < D; ++l) a[1 + l] = x[l] - rk[l];
+      double zl = 0.0;
+      for (int l = 0; l < Q; ++l) {
+        double v = 0.0;
+#pragma unroll
+        for (int p = 0; p < KC::N1; ++p) v = fma(sBZ[l * KC::N1 + p], a[p], v);
+        zl = fma(zweight(P, l), trunc_L(v, P.C_z), zl);
+      }
+      const double Sm = BYs[2 * m] + f_eval(P, BYs[2 * m + 1], zl) * dt;
+#pragma unroll
+      for (int p = 0; p < KC::N1; ++p) ry[p] = fma(a[p], Sm, ry[p]);
+    }
+#pragma unroll
+    for (int p = 0; p < KC::N1; ++p) {
+      double v = ry[p];
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) v = v + __shfl_down_sync(0xffffffffu, v, off);
+      if ((tid & 31) == 0) sWarp[(tid >> 5) * KC::N1 + p] = v;
+    }
+    __syncthreads();
+    if (tid < KC::N1) {
+      double v = sWarp[tid];
+      for (int w = 1; w < kThreads / 32; ++w) v = v + sWarp[w * KC::N1 + tid];
+      sRY[tid] = v;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      if (ok) {
+        chol_solve<KC::N1>(sL, sRY, sBY);
+      } else {
+        sBY[0] = sRY[0] / (double)M;
+        for (int p = 1; p < KC::N1; ++p) sBY[p] = 0.0;
+        atomicAdd(P.lp0_count, 1ull);
+      }
+    }
+    __syncthreads();
+    double* dst = P.table + ((size_t)i * (size_t)P.K_pad + k) * (size_t)KC::NBP;
+    for (int b = tid; b < KC::NBP; b += kThreads)
+      dst[b] = (b < KC::N1) ? sBY[b] : ((b < KC::NB) ? sBZ[b - KC::N1] : 0.0);
+    __syncthreads();
+  }
+}
+
+}  // namespace srk

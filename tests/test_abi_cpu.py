@@ -1,0 +1,82 @@
+"""C-ABI checks that need no GPU: the library builds for sm_100a, loads, and
+exports every symbol include/*.h declares; the pure-host shard planner
+(docs/layout.md) tiles the cell range."""
+import os
+import re
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_symbols():
+    names = set()
+    for f in os.listdir(os.path.join(ROOT, "include")):
+        src = open(os.path.join(ROOT, "include", f)).read()
+        src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+        names |= set(re.findall(r"\b(srmdp_\w+)\s*\(", src))
+    return names
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_2407_21085_b200 import build
+    build.build()
+    from paper_2407_21085_b200 import srmdp
+    return srmdp
+
+
+def test_header_declares_the_boundary():
+    names = declared_symbols()
+    for n in ("srmdp_create", "srmdp_solve", "srmdp_coeffs", "srmdp_eval", "srmdp_destroy",
+              "srmdp_stats", "srmdp_nccl_unique_id", "srmdp_shard_plan", "srmdp_debug_trace"):
+        assert n in names
+
+
+def test_library_exports_every_declared_symbol(lib):
+    so = lib.library()
+    for n in declared_symbols():
+        assert hasattr(so, n), n
+    out = subprocess.run(["nm", "-D", "--defined-only", lib.LIB_PATH], capture_output=True, text=True).stdout
+    exported = set(re.findall(r"\b(srmdp_\w+)$", out, flags=re.M))
+    assert declared_symbols() <= exported
+    # the binding declares exactly the header's functions
+    assert set(lib.SIGNATURES) == declared_symbols()
+
+
+def test_built_for_sm100a(lib):
+    out = subprocess.run(["cuobjdump", "--list-elf", lib.LIB_PATH], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+    assert "sm_100a" in lib.srmdp_build_info()
+
+
+@pytest.mark.parametrize("K,world", [(1, 1), (10, 1), (10, 3), (15625, 8), (7, 8), (524288, 8)])
+def test_shard_plan_tiles_cells(lib, K, world):
+    ranges = [lib.srmdp_shard_plan(K, world, r) for r in range(world)]
+    chunk, K_pad = ranges[0][2], ranges[0][3]
+    assert K_pad == chunk * world and K_pad >= K and K_pad - K < world
+    pos = 0
+    for r, (b, e, c, kp) in enumerate(ranges):
+        assert (c, kp) == (chunk, K_pad)
+        assert b == min(r * chunk, K) and e == min((r + 1) * chunk, K)
+        assert b == pos or (b == K and e == K)
+        pos = e
+    assert pos == K
+
+
+def test_shard_plan_rejects_bad_args(lib):
+    with pytest.raises(lib.SrmdpError):
+        lib.srmdp_shard_plan(0, 1, 0)
+    with pytest.raises(lib.SrmdpError):
+        lib.srmdp_shard_plan(10, 2, 2)
+
+
+def test_product_does_not_import_oracle():
+    """The product package never references the oracle (no CPU fallback)."""
+    pkg = os.path.join(ROOT, "paper_2407_21085_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
+                src = open(os.path.join(dirpath, f)).read()
+                assert "import oracle" not in src and "srmdp_oracle" not in src and "or_solve" not in src, f
