@@ -88,6 +88,7 @@ def lib():
             "or_ols_qr": (ctypes.c_int, [_PD, _I64, ctypes.c_int, _PD, ctypes.c_int, _PD]),
             "or_step": (_I64, [P, _PD, ctypes.c_int, _I64, _I64, _I64]),
             "or_solve": (_I64, [P, _PD]),
+            "or_step_cells": (_I64, [P, _PD, ctypes.c_int, ctypes.POINTER(_I64), _I64]),
             "or_eval": (None, [P, _PD, ctypes.c_int, _I64, _PD, _PD, _PD]),
             "or_num_threads": (ctypes.c_int, []),
         }
@@ -150,6 +151,10 @@ class Problem:
         if k_end is None:
             k_end = self.K
         return int(lib().or_step(self.ref, _dptr(table), i, k_begin, k_end, k_stride))
+
+    def step_cells(self, table, i, cells):
+        c = np.ascontiguousarray(np.asarray(cells, dtype=np.int64))
+        return int(lib().or_step_cells(self.ref, _dptr(table), i, c.ctypes.data_as(ctypes.POINTER(_I64)), c.size))
 
     def eval(self, table, i, x, want_z=True):
         x = np.ascontiguousarray(x, dtype=np.float64).reshape(-1, self.d)

@@ -583,6 +583,13 @@ int64_t or_step(const or_problem* p, double* table, int i,
   return fb;
 }
 
+int64_t or_step_cells(const or_problem* p, double* table, int i, const int64_t* cells, int64_t n) {
+  int64_t fb = 0;
+#pragma omp parallel for schedule(dynamic, 1) reduction(+ : fb)
+  for (int64_t t = 0; t < n; t++) fb += step_cell(p, table, i, cells[t]);
+  return fb;
+}
+
 /* Backward iteration i = N-1 .. 0. */
 int64_t or_solve(const or_problem* p, double* table) {
   int64_t K = or_num_cells(p), fb = 0;

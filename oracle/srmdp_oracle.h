@@ -85,6 +85,8 @@ int    or_ols_qr(double* A, int64_t M, int n, double* S, int nrhs, double* beta)
  * reading table[j][*] for j > i. Returns the number of LP0 fallbacks. */
 int64_t or_step(const or_problem* p, double* table, int i,
                 int64_t k_begin, int64_t k_end, int64_t k_stride);
+/* Same for an explicit list of cells (used to evaluate only visited cells). */
+int64_t or_step_cells(const or_problem* p, double* table, int i, const int64_t* cells, int64_t n);
 int64_t or_solve(const or_problem* p, double* table);
 /* Evaluate the truncated approximations at time i (i == N: g, z ignored). */
 void   or_eval(const or_problem* p, const double* table, int i, int64_t n,

@@ -39,7 +39,7 @@ __global__ void eval_kernel(const DevProblem P, const int i, const int64_t n, co
     for (int l = 0; l < Q; ++l) {
       double w = 0.0;
 #pragma unroll
-      for (int p = 0; p <= D; ++p) w = fma(__ldg(blk + (1 + l) * KC::N1 + p), a[p], w);
+      for (int p = 0; p <= D; ++p) w = fma(__ldg(blk + KC::NH + l * KC::N1 + p), a[p], w);
       zs[t * Q + l] = trunc_L(w, P.C_z);
     }
   }

@@ -284,15 +284,25 @@ static void bounds(double C_g, double C_f, double L_f, int q, double T, int N, d
   *ok = dt * Lf2 <= 1.0 / (12.0 * q);
 }
 
+// Inside stream capture an event must be an external record node to time
+// the captured kernel; outside capture a plain record.
+static cudaError_t record_event(srmdp_t* h, cudaEvent_t e) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  cudaError_t r = cudaStreamIsCapturing(h->stream, &cs);
+  if (r != cudaSuccess) return r;
+  return (cs == cudaStreamCaptureStatusActive) ? cudaEventRecordWithFlags(e, h->stream, cudaEventRecordExternal)
+                                               : cudaEventRecord(e, h->stream);
+}
+
 static srmdp_status enqueue_sweep(srmdp_t* h) {
   const bool timed = h->cfg.flags & SRMDP_FLAG_TIME_KERNELS;
   CK(h, cudaMemsetAsync(h->d_lp0, 0, sizeof(unsigned long long), h->stream), "memset");
   const int64_t nk = h->k_end - h->k_begin;
   for (int i = h->N - 1; i >= 0; --i) {
-    if (timed) CK(h, cudaEventRecordWithFlags(h->ev[2 * i], h->stream, cudaEventRecordExternal), "event");
+    if (timed) CK(h, record_event(h, h->ev[2 * i]), "event");
     if (nk > 0) h->ops->step(h->dp, i, h->k_begin, nk, h->grid, h->smem, h->stream);
     CK(h, cudaGetLastError(), "step kernel launch");
-    if (timed) CK(h, cudaEventRecordWithFlags(h->ev[2 * i + 1], h->stream, cudaEventRecordExternal), "event");
+    if (timed) CK(h, record_event(h, h->ev[2 * i + 1]), "event");
     if (h->cfg.world > 1) {
       double* slice = h->d_table + (size_t)i * h->K_pad * h->B_pad;
       const size_t cnt = (size_t)h->chunk * h->B_pad;
@@ -318,7 +328,7 @@ extern "C" srmdp_status srmdp_create(const srmdp_config* cfg, srmdp_t** out) {
   h->K = 1;
   for (int l = 0; l < h->d; ++l) h->K *= h->C;
   h->B = (h->q + 1) * (h->d + 1);
-  h->B_pad = h->B + (h->B & 1);
+  h->B_pad = block_stride(h->d, h->q);
   int64_t plan[4];
   srmdp_shard_plan(h->K, cfg->world, cfg->rank, plan);
   h->k_begin = plan[0]; h->k_end = plan[1]; h->chunk = plan[2]; h->K_pad = plan[3];
@@ -370,8 +380,10 @@ extern "C" srmdp_status srmdp_create(const srmdp_config* cfg, srmdp_t** out) {
   cudaMemcpy(h->d_params, h->params.data(), h->params.size() * sizeof(double), cudaMemcpyHostToDevice);
   cudaMemcpy(h->d_tabs, tabs.data(), tabs.size() * sizeof(double), cudaMemcpyHostToDevice);
 
-  // launch configuration: persistent CTAs, (B_m, Y1_m) in smem when M <= 4096
-  const bool by_smem = h->M <= 4096;
+  // launch configuration: persistent CTAs; the pass-1 pairs (B_m, Y1_m) go to a
+  // per-CTA global scratch (L2-resident) so shared memory stays small and the
+  // L1 keeps room for the prefetched coefficient blocks (3 CTAs/SM)
+  const bool by_smem = false;
   e = h->ops->prepare(h->C, h->M, by_smem, &h->smem, &h->ctas);
   if (e != cudaSuccess || h->ctas < 1) {
     if (e == cudaSuccess) h->err = "step kernel does not fit on an SM";
@@ -406,6 +418,12 @@ extern "C" srmdp_status srmdp_create(const srmdp_config* cfg, srmdp_t** out) {
   P.f_cq = (2.0 + (double)h->q) / (2.0 * (double)h->q);
   P.key0 = (uint32_t)(cfg->seed & 0xffffffffu);
   P.key1 = (uint32_t)(cfg->seed >> 32);
+  for (int r = 0; r < 10; ++r) {   // Philox round keys (docs/streams.md §1)
+    P.rkey.k0[r] = P.key0 + (uint32_t)r * 0x9E3779B9u;
+    P.rkey.k1[r] = P.key1 + (uint32_t)r * 0xBB67AE85u;
+  }
+  P.inv_dt = 1.0 / P.dt;
+  P.C_z_safe = h->C_z * (1.0 - 0x1p-40);
   P.dyn_params = h->d_params;
   P.theta = h->d_params + nd;
   P.g_params = h->d_params + goff;
@@ -497,8 +515,13 @@ extern "C" srmdp_status srmdp_coeffs(const srmdp_t* h, int i, int basis, double*
   }
   CK(h, cudaSetDevice(h->cfg.device), "cudaSetDevice");
   const double* src = h->d_table + (size_t)i * h->K_pad * h->B_pad;
-  CK(h, cudaMemcpy2DAsync(out, h->B * sizeof(double), src, h->B_pad * sizeof(double), h->B * sizeof(double),
+  // device block [Y | W | S | pad | Z_1..Z_q | pad] -> host [Y | Z_1..Z_q]
+  const size_t n1 = (size_t)(h->d + 1), hot = (size_t)hot_len(h->d);
+  CK(h, cudaMemcpy2DAsync(out, h->B * sizeof(double), src, h->B_pad * sizeof(double), n1 * sizeof(double),
                           (size_t)h->K, cudaMemcpyDeviceToHost, h->stream),
+     "coeffs copy");
+  CK(h, cudaMemcpy2DAsync(out + n1, h->B * sizeof(double), src + hot, h->B_pad * sizeof(double),
+                          (h->B - n1) * sizeof(double), (size_t)h->K, cudaMemcpyDeviceToHost, h->stream),
      "coeffs copy");
   CK(h, cudaStreamSynchronize(h->stream), "coeffs copy");
   if (basis == 0) {  // raw alpha of P:718: alpha_0 = beta_0 - sum_j beta_j r_j

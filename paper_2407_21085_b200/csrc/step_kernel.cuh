@@ -29,7 +29,8 @@ template <int D, int Q>
 struct KCfg {
   static constexpr int N1 = D + 1;
   static constexpr int NB = (Q + 1) * N1;           // B
-  static constexpr int NBP = NB + (NB & 1);         // B_pad
+  static constexpr int NH = hot_len(D);             // hot part [Y | W | S | pad]
+  static constexpr int NBP = block_stride(D, Q);    // device block stride (doubles)
   static constexpr int NG = N1 * (N1 + 1) / 2;      // Gram entries (upper, incl. diag)
   static constexpr int NZ = Q * N1;                 // Z right-hand-side entries
   static constexpr int E = NG + NZ;
@@ -37,7 +38,6 @@ struct KCfg {
   static constexpr int PAIRS = E * S;
   static constexpr int NACC = (PAIRS + kThreads - 1) / kThreads;
   static constexpr int ROW = (1 + D + Q) | 1;       // [1 | x - r_k | S dW/dt], odd stride
-  static constexpr bool KEEP_DWI = (Q <= 8);
   static constexpr bool UNROLL_GATHER = (NB <= 128);
 };
 
@@ -60,85 +60,118 @@ struct SmemLayout {
   }
 };
 
+// Exact evaluation of the q Z blocks: zlin = sum_l w_l T_{C_z}(beta^{Z_l} . a).
+template <int D, int Q>
+__device__ __forceinline__ double zlin_exact(const DevProblem& P, const double* __restrict__ blk, const double (&a)[D + 1]) {
+  using KC = KCfg<D, Q>;
+  double zl = 0.0;
+#pragma unroll 1
+  for (int l = 0; l < Q; ++l) {
+    const double* bz = blk + KC::NH + l * KC::N1;
+    double v = 0.0;
+#pragma unroll
+    for (int p = 0; p <= D; ++p) v = fma(__ldg(bz + p), a[p], v);
+    zl = fma(zweight(P, l), trunc_L(v, P.C_z), zl);
+  }
+  return zl;
+}
+
 // Evaluate the fitted block of a cell at centered coordinates a = (1, x - r):
 // y = T_{C_y}(beta^Y . a), zlin = sum_l w_l T_{C_z}(beta^{Z_l} . a).
+// Fast path (one 128-byte line for d <= 6): when S * max(1, max_p |a_p|) is
+// below C_z no component can be truncated, so zlin = W . a (same value up to
+// rounding order, reading R23); otherwise the exact per-component path.
 template <int D, int Q>
 __device__ __forceinline__ void eval_block(const DevProblem& P, const double* __restrict__ blk,
                                            const double (&a)[D + 1], double& y, double& zlin) {
   using KC = KCfg<D, Q>;
-  if constexpr (KC::UNROLL_GATHER) {
-    double out[Q + 1];
+  constexpr int NHOT = 2 * KC::N1 + 1;
+  double yv = 0.0, wv = 0.0, S = 0.0;
+  const double2* b2 = reinterpret_cast<const double2*>(blk);
 #pragma unroll
-    for (int o = 0; o <= Q; ++o) out[o] = 0.0;
-    const double2* b2 = reinterpret_cast<const double2*>(blk);
+  for (int u = 0; u < (NHOT + 1) / 2; ++u) {
+    const double2 v = __ldg(b2 + u);
 #pragma unroll
-    for (int u = 0; u < KC::NBP / 2; ++u) {
-      const double2 v = __ldg(b2 + u);
-      const int e0 = 2 * u, e1 = 2 * u + 1;
-      out[e0 / KC::N1] = fma(v.x, a[e0 % KC::N1], out[e0 / KC::N1]);
-      if (e1 < KC::NB) out[e1 / KC::N1] = fma(v.y, a[e1 % KC::N1], out[e1 / KC::N1]);
+    for (int h = 0; h < 2; ++h) {
+      const int e = 2 * u + h;
+      const double c = h ? v.y : v.x;
+      if (e < KC::N1) yv = fma(c, a[e], yv);
+      else if (e < 2 * KC::N1) wv = fma(c, a[e - KC::N1], wv);
+      else if (e == 2 * KC::N1) S = c;
     }
-    y = trunc_L(out[0], P.C_y);
-    double zl = 0.0;
-#pragma unroll
-    for (int l = 0; l < Q; ++l) zl = fma(zweight(P, l), trunc_L(out[1 + l], P.C_z), zl);
-    zlin = zl;
-  } else {
-    double acc = 0.0;
-#pragma unroll
-    for (int p = 0; p <= D; ++p) acc = fma(__ldg(blk + p), a[p], acc);
-    y = trunc_L(acc, P.C_y);
-    double zl = 0.0;
-#pragma unroll 1
-    for (int l = 0; l < Q; ++l) {
-      const double* bz = blk + (1 + l) * KC::N1;
-      double v = 0.0;
-#pragma unroll
-      for (int p = 0; p <= D; ++p) v = fma(__ldg(bz + p), a[p], v);
-      zl = fma(zweight(P, l), trunc_L(v, P.C_z), zl);
-    }
-    zlin = zl;
   }
+  y = trunc_L(yv, P.C_y);
+  // conservative max(1, max_p |a_p|) from the high words (integer pipe)
+  int hm = 0x3ff00000;
+#pragma unroll
+  for (int p = 1; p <= D; ++p) hm = max(hm, __double2hiint(a[p]) & 0x7fffffff);
+  const double amax = __hiloint2double(hm, 0xffffffff);
+  if (S * amax <= P.C_z_safe) zlin = wv;
+  else zlin = zlin_exact<D, Q>(P, blk, a);
 }
 
-// One path of cloud (i,k): start point x_i, then the Euler chain with the
-// multistep response. Returns B = S_{Y,i+1}(x_i) = g(x_N) + sum_{j>i} f_j dt
-// (eq. PsiM), Y1 = y_{i+1}(x_{i+1}) and dW_i.
+// L1 prefetch of a coefficient block (every 128-byte line it spans).
+template <int NHOT>
+__device__ __forceinline__ void prefetch_block(const double* blk) {
+#pragma unroll
+  for (int off = 0; off < NHOT * 8; off += 128) asm volatile("prefetch.global.L1 [%0];" ::"l"((const char*)blk + off));
+}
+
+// One path of cloud (i,k), pass 1. Writes the design row (1, x_i - r_k) and
+// dW_i into `row` (shared memory) as soon as they exist, so neither stays in
+// registers across the Euler chain. Returns B = S_{Y,i+1}(x_i) = g(x_N) +
+// sum_{j>i} f_j dt (eq. PsiM) and Y1 = y_{i+1}(x_{i+1}).
+// Software pipeline: the block of X_{j+1} is prefetched into L1, then the
+// increments and Euler step of X_{j+2} are computed (FP64-heavy, independent
+// of the gather), then the block is evaluated.
 template <int D, int Q>
 __device__ __forceinline__ void simulate_path(const DevProblem& P, const double* sFe, const double* sEdge,
                                               const double* sCen, const int (&cc)[D], int i, uint32_t k,
-                                              uint32_t m, double (&x)[D], double& Bout, double& Y1out,
-                                              double (&dWi)[Q]) {
+                                              uint32_t m, double* row, double& Bout, double& Y1out) {
   using KC = KCfg<D, Q>;
-  start_point<D>(P, sFe, sEdge, cc, i, k, m, x);
-  double X[D];
+  double Xn[D];
+  start_point<D>(P, sFe, sEdge, cc, i, k, m, Xn);
+  row[0] = 1.0;
 #pragma unroll
-  for (int l = 0; l < D; ++l) X[l] = x[l];
+  for (int l = 0; l < D; ++l) row[1 + l] = Xn[l] - sCen[cc[l]];
+  {
+    double dW[Q], X1[D];
+    brownian<Q>(P, i, i, k, m, dW);
+#pragma unroll
+    for (int l = 0; l < Q; ++l) row[1 + D + l] = dW[l];
+    euler<D, Q>(P, Xn, dW, X1);
+#pragma unroll
+    for (int l = 0; l < D; ++l) Xn[l] = X1[l];
+  }
   double acc = 0.0, zlin = 0.0, Y1 = 0.0, yv = 0.0;
   const int N = P.N;
+#pragma unroll 1
   for (int j = i; j < N; ++j) {
-    double dW[Q];
-    brownian<Q>(P, i, j, k, m, dW);
-    if (KC::KEEP_DWI && j == i) {
-#pragma unroll
-      for (int l = 0; l < Q; ++l) dWi[l] = dW[l];
-    }
-    double Xn[D];
-    euler<D, Q>(P, X, dW, Xn);
+    // Xn = X_{j+1}
     double zn = 0.0;
     if (j + 1 < N) {
-      // locate X_{j+1} ((A_Strat.), docs/streams.md §6) and gather its block
       uint32_t kn = 0;
+      int c[D];
+#pragma unroll
+      for (int l = 0; l < D; ++l) {
+        c[l] = locate1(Xn[l], P.L, P.inv_delta, P.C);
+        kn = kn * (uint32_t)P.C + (uint32_t)c[l];
+      }
+      const double* blk = P.table + ((size_t)(j + 1) * (size_t)P.K_pad + kn) * (size_t)KC::NBP;
+      prefetch_block<2 * KC::N1 + 1>(blk);
+      double Xnn[D];
+      {
+        double dW[Q];
+        brownian<Q>(P, i, j + 1, k, m, dW);       // increments of step j+1 (independent of the gather)
+        euler<D, Q>(P, Xn, dW, Xnn);
+      }
       double a[D + 1];
       a[0] = 1.0;
 #pragma unroll
-      for (int l = 0; l < D; ++l) {
-        const int c = locate1(Xn[l], P.L, P.inv_delta, P.C);
-        kn = kn * (uint32_t)P.C + (uint32_t)c;
-        a[1 + l] = Xn[l] - sCen[c];
-      }
-      const double* blk = P.table + ((size_t)(j + 1) * (size_t)P.K_pad + kn) * (size_t)KC::NBP;
-      eval_block<D, Q>(P, blk, a, yv, zn);
+      for (int l = 0; l < D; ++l) a[1 + l] = Xn[l] - sCen[c[l]];
+      eval_block<D, Q>(P, blk, a, yv, zn);        // y_{j+1}(x_{j+1}), z_{j+1}(x_{j+1})
+#pragma unroll
+      for (int l = 0; l < D; ++l) Xn[l] = Xnn[l];
     } else {
       yv = g_eval<D>(P, Xn);                      // y_N := g
     }
@@ -149,12 +182,9 @@ __device__ __forceinline__ void simulate_path(const DevProblem& P, const double*
       acc = acc + fdt;
     }
     zlin = zn;
-#pragma unroll
-    for (int l = 0; l < D; ++l) X[l] = Xn[l];
   }
   Bout = yv + acc;                                 // g(x_N) + sum
   Y1out = Y1;
-  if (!KC::KEEP_DWI) brownian<Q>(P, i, i, k, m, dWi);
 }
 
 // Cholesky of the symmetric n x n matrix in A (full storage), lower factor in
@@ -197,7 +227,7 @@ __device__ void chol_solve(const double* L, const double* r, double* b) {
 }
 
 template <int D, int Q>
-__global__ void __launch_bounds__(kThreads, 2)
+__global__ void __launch_bounds__(kThreads, 3)
 step_kernel(const DevProblem P, const int i, const int64_t k_begin, const int64_t nk) {
   using KC = KCfg<D, Q>;
   using SL = SmemLayout<D, Q>;
@@ -255,9 +285,6 @@ step_kernel(const DevProblem P, const int i, const int64_t k_begin, const int64_
 #pragma unroll
       for (int l = D - 1; l >= 0; --l) { cc[l] = (int)(r % (uint32_t)C); r /= (uint32_t)C; }
     }
-    double rk[D];
-#pragma unroll
-    for (int l = 0; l < D; ++l) rk[l] = sCen[cc[l]];
 
     // ---------------- pass 1: paths, Gram and Z right-hand sides ----------
     double acc[KC::NACC];
@@ -267,14 +294,12 @@ step_kernel(const DevProblem P, const int i, const int64_t k_begin, const int64_
       const int64_t m = m0 + tid;
       const int nrows = (int)((M - m0) < kThreads ? (M - m0) : kThreads);
       if (m < M) {
-        double x[D], dWi[Q], Bv, Y1;
-        simulate_path<D, Q>(P, sFe, sEdge, sCen, cc, i, k, (uint32_t)m, x, Bv, Y1, dWi);
         double* row = sRows + tid * KC::ROW;
-        row[0] = 1.0;
+        double Bv, Y1;
+        simulate_path<D, Q>(P, sFe, sEdge, sCen, cc, i, k, (uint32_t)m, row, Bv, Y1);
+        const double sc = Bv * P.inv_dt;
 #pragma unroll
-        for (int l = 0; l < D; ++l) row[1 + l] = x[l] - rk[l];
-#pragma unroll
-        for (int l = 0; l < Q; ++l) row[1 + D + l] = (Bv * dWi[l]) / dt;   // S_{Z,i} = S_{Y,i+1} w / dt
+        for (int l = 0; l < Q; ++l) row[1 + D + l] = row[1 + D + l] * sc;   // S_{Z,i} = S_{Y,i+1} dW_i / dt
         BYs[2 * m] = Bv;
         BYs[2 * m + 1] = Y1;
       }
@@ -334,7 +359,7 @@ step_kernel(const DevProblem P, const int i, const int64_t k_begin, const int64_
       start_point<D>(P, sFe, sEdge, cc, i, k, (uint32_t)m, x);
       a[0] = 1.0;
 #pragma unroll
-      for (int l = 0; l < D; ++l) a[1 + l] = x[l] - rk[l];
+      for (int l = 0; l < D; ++l) a[1 + l] = x[l] - sCen[cc[l]];
       double zl = 0.0;
       for (int l = 0; l < Q; ++l) {
         double v = 0.0;
@@ -370,9 +395,30 @@ step_kernel(const DevProblem P, const int i, const int64_t k_begin, const int64_
       }
     }
     __syncthreads();
+    // certificate of the hot part: W = sum_l w_l beta^{Z_l}, S = max_l ||beta^{Z_l}||_1
+    if (tid < KC::N1) {
+      double wsum = 0.0;
+      for (int l = 0; l < Q; ++l) wsum = fma(zweight(P, l), sBZ[l * KC::N1 + tid], wsum);
+      sRY[tid] = wsum;
+    } else if (tid == KC::N1) {
+      double smax = 0.0;
+      for (int l = 0; l < Q; ++l) {
+        double t = 0.0;
+        for (int p = 0; p < KC::N1; ++p) t += fabs(sBZ[l * KC::N1 + p]);
+        smax = fmax(smax, t);
+      }
+      sWarp[0] = smax;
+    }
+    __syncthreads();
     double* dst = P.table + ((size_t)i * (size_t)P.K_pad + k) * (size_t)KC::NBP;
-    for (int b = tid; b < KC::NBP; b += kThreads)
-      dst[b] = (b < KC::N1) ? sBY[b] : ((b < KC::NB) ? sBZ[b - KC::N1] : 0.0);
+    for (int b = tid; b < KC::NBP; b += kThreads) {
+      double v = 0.0;
+      if (b < KC::N1) v = sBY[b];
+      else if (b < 2 * KC::N1) v = sRY[b - KC::N1];
+      else if (b == 2 * KC::N1) v = sWarp[0];
+      else if (b >= KC::NH && b < KC::NH + KC::NZ) v = sBZ[b - KC::NH];
+      dst[b] = v;
+    }
     __syncthreads();
   }
 }
