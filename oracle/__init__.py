@@ -26,7 +26,7 @@ DYN = {"bm": 0, "gbm": 1, "affine": 2}
 FKIND = {"zero": 0, "linear": 1, "paper": 2}
 GKIND = {"affine": 0, "paper": 1}
 
-CFLAGS = ["-O2", "-ffp-contract=off", "-fno-fast-math", "-fopenmp", "-fPIC", "-shared", "-std=c11"]
+CFLAGS = ["-O2", "-ffp-contract=off", "-fno-fast-math", "-fopenmp", "-fPIC", "-shared", "-std=gnu11", "-pthread"]
 
 
 def build(force: bool = False) -> str:
@@ -72,6 +72,8 @@ def lib():
             "or_dm_log": (_D, [_D]),
             "or_dm_exp": (_D, [_D]),
             "or_dm_sincospi2": (None, [_D, _PD, _PD]),
+            "or_dm_log_series": (_D, [_D]),
+            "or_dm_sincospi2_series": (None, [_D, _PD, _PD]),
             "or_F": (_D, [_D, _D]),
             "or_inv_cdf_cond": (_D, [_D, _D, _D, _D]),
             "or_locate1": (ctypes.c_int, [_D, ctypes.c_int, _D]),
@@ -247,6 +249,16 @@ def u01(w):
 
 def dm_log(x):
     return lib().or_dm_log(float(x))
+
+
+def dm_log_series(x):
+    return lib().or_dm_log_series(float(x))
+
+
+def dm_sincospi2_series(u):
+    s, c = _D(), _D()
+    lib().or_dm_sincospi2_series(float(u), ctypes.byref(s), ctypes.byref(c))
+    return s.value, c.value
 
 
 def dm_exp(x):

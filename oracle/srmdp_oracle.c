@@ -15,7 +15,7 @@
  * Pins (tests/test_oracle_*.py, all `-m "not gpu"`):
  *   philox            Random123/cuRAND known-answer vectors
  *   or_u01            exact extremes 2^-53, 1-2^-53
- *   dm_log/exp/sincos mpmath at <= 2 ulp
+ *   dm_log/exp/sincos mpmath at <= 3 ulp (path and reference/series versions)
  *   F, inv_cdf_cond   closed forms (F(ln 3)=0.75, medians), KS vs analytic CDF
  *   locate            SPEC-style examples, membership of every sample
  *   euler             closed-form random walk / ODE examples
@@ -31,6 +31,7 @@
 #include "srmdp_oracle.h"
 
 #include <math.h>
+#include <pthread.h>
 #include <stdlib.h>
 #include <string.h>
 #ifdef _OPENMP
@@ -79,7 +80,7 @@ static void draw_block(const or_problem* p, uint32_t c0, int64_t m, int64_t k, i
 static const double LN2_HI = 0x1.62e42fee00000p-1;
 static const double LN2_LO = 0x1.a39ef35793c76p-33;
 
-double or_dm_log(double x) {
+double or_dm_log_series(double x) {
   static const double LG[11] = {0.0,
       0x1.5555555555555p-1, 0x1.999999999999ap-2, 0x1.2492492492492p-2,
       0x1.c71c71c71c71cp-3, 0x1.745d1745d1746p-3, 0x1.3b13b13b13b14p-3,
@@ -127,7 +128,7 @@ double or_dm_exp(double x) {
   return ldexp(P, (int)kf);
 }
 
-void or_dm_sincospi2(double u, double* s, double* c) {
+void or_dm_sincospi2_series(double u, double* s, double* c) {
   static const double S[9] = {
       0x1.921fb54442d18p+0, -0x1.4abbce625be53p-1, 0x1.466bc6775aae2p-4,
       -0x1.32d2cce62bd86p-8, 0x1.50783487ee782p-13, -0x1.e3074fde8871fp-19,
@@ -154,6 +155,78 @@ void or_dm_sincospi2(double u, double* s, double* c) {
     case 2: *s = -sn; *c = -cs; break;
     default: *s = -cs; *c = sn; break;
   }
+}
+
+/* Tables of docs/detmath.md, built once from the reference functions. */
+static double LOGT_INVC[128], LOGT_LT[128], SCT_S[128], SCT_C[128];
+static pthread_once_t tables_once = PTHREAD_ONCE_INIT;
+
+static void build_tables(void) {
+  for (int j = 0; j < 128; j++) {
+    if (j == 0 || j == 127) {
+      LOGT_INVC[j] = 1.0;
+      LOGT_LT[j] = 0.0;
+    } else {
+      double c = 1.0 + (((double)j + 0.5) / 128.0);
+      if (j >= 53) c = c * 0.5;
+      LOGT_INVC[j] = 1.0 / c;
+      LOGT_LT[j] = -or_dm_log_series(LOGT_INVC[j]);
+    }
+    or_dm_sincospi2_series((double)j / 128.0, &SCT_S[j], &SCT_C[j]);
+  }
+}
+
+void or_init_tables(void) { pthread_once(&tables_once, build_tables); }
+
+/* dm_log (path function, docs/detmath.md): table-driven, division-free. */
+double or_dm_log(double x) {
+  static const double A[10] = {0.0, 0.0,
+      -0x1.0000000000000p-1, 0x1.5555555555555p-2, -0x1.0000000000000p-2, 0x1.999999999999ap-3,
+      -0x1.5555555555555p-3, 0x1.2492492492492p-3, -0x1.0000000000000p-3, 0x1.c71c71c71c71cp-4};
+  or_init_tables();
+  if (x != x || x < 0.0) return NAN;
+  if (x == 0.0) return -INFINITY;
+  if (isinf(x)) return INFINITY;
+  int k = 0;
+  if (x < 0x1p-1022) { x = x * 0x1p54; k = -54; }
+  uint64_t b;
+  memcpy(&b, &x, 8);
+  k = k + (int)(b >> 52) - 1023;
+  uint64_t mb = b & 0x000fffffffffffffull;
+  int j = (int)(mb >> 45);
+  uint64_t m1 = mb | 0x3ff0000000000000ull;
+  double m;
+  memcpy(&m, &m1, 8);
+  if (j >= 53) { m = m * 0.5; k = k + 1; }
+  double r = fma(m, LOGT_INVC[j], -1.0);
+  double r2 = r * r;
+  double p = A[9];
+  for (int n = 8; n >= 2; n--) p = fma(p, r, A[n]);
+  double l1 = fma(r2, p, r);
+  double kd = (double)k;
+  return ((kd * LN2_HI) + LOGT_LT[j]) + (l1 + (kd * LN2_LO));
+}
+
+/* dm_sincospi2 (path function, docs/detmath.md): (sin 2 pi u, cos 2 pi u), 0 <= u < 1. */
+void or_dm_sincospi2(double u, double* s, double* c) {
+  static const double Pk[5] = {0x1.921fb54442d18p-5, -0x1.4abbce625be53p-16, 0x1.466bc6775aae2p-29,
+                               -0x1.32d2cce62bd86p-43, 0x1.50783487ee782p-58};
+  static const double Qk[5] = {0x1.0000000000000p+0, -0x1.3bd3cc9be45dep-10, 0x1.03c1f081b5ac4p-22,
+                               -0x1.55d3c7e3cbffap-36, 0x1.e1f506891babbp-51};
+  or_init_tables();
+  double t = u * 128.0;
+  int j = (int)floor(t);
+  double g = t - (double)j;
+  double g2 = g * g;
+  double ps = Pk[4];
+  for (int k = 3; k >= 0; k--) ps = fma(ps, g2, Pk[k]);
+  double sg = g * ps;
+  double pc = Qk[4];
+  for (int k = 3; k >= 0; k--) pc = fma(pc, g2, Qk[k]);
+  double cg = pc;
+  double Sj = SCT_S[j], Cj = SCT_C[j];
+  *s = fma(Sj, cg, Cj * sg);
+  *c = fma(Cj, cg, -(Sj * sg));
 }
 
 /* ------------------------------------------------------------------ */
@@ -576,6 +649,7 @@ static int64_t step_cell(const or_problem* p, double* table, int i, int64_t k) {
 int64_t or_step(const or_problem* p, double* table, int i,
                 int64_t k_begin, int64_t k_end, int64_t k_stride) {
   int64_t fb = 0;
+  or_init_tables();
   if (k_stride < 1) k_stride = 1;
   int64_t cnt = (k_end > k_begin) ? (k_end - k_begin + k_stride - 1) / k_stride : 0;
 #pragma omp parallel for schedule(static) reduction(+ : fb)
@@ -585,6 +659,7 @@ int64_t or_step(const or_problem* p, double* table, int i,
 
 int64_t or_step_cells(const or_problem* p, double* table, int i, const int64_t* cells, int64_t n) {
   int64_t fb = 0;
+  or_init_tables();
 #pragma omp parallel for schedule(dynamic, 1) reduction(+ : fb)
   for (int64_t t = 0; t < n; t++) fb += step_cell(p, table, i, cells[t]);
   return fb;

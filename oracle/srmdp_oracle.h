@@ -45,9 +45,12 @@ typedef struct {
 /* --- primitives (docs/streams.md, docs/detmath.md) --- */
 void   or_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4]);
 double or_u01(uint64_t w);
-double or_dm_log(double x);
+double or_dm_log(double x);                              /* path function (table-driven) */
+double or_dm_log_series(double x);                       /* reference function */
 double or_dm_exp(double x);
-void   or_dm_sincospi2(double u, double* s, double* c);
+void   or_dm_sincospi2(double u, double* s, double* c);  /* path function (table-driven) */
+void   or_dm_sincospi2_series(double u, double* s, double* c);
+void   or_init_tables(void);
 double or_F(double mu, double x);
 double or_inv_cdf_cond(double mu, double lo, double hi, double U);
 int    or_locate1(double x, int C, double L);

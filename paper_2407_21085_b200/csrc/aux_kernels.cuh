@@ -20,7 +20,7 @@ __global__ void eval_kernel(const DevProblem P, const int i, const int64_t n, co
     ys[t] = g_eval<D>(P, x);
     return;
   }
-  const double* cen = P.tabs + 2 * (P.C + 1);
+  const double* cen = P.tabs + 2 * (P.C + 1);   // read through L1 (no draws here)
   uint32_t kn = 0;
   double a[D + 1];
   a[0] = 1.0;
@@ -53,8 +53,7 @@ __global__ void trace_kernel(const DevProblem P, const int i, const uint32_t k, 
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= n) return;
   const uint32_t m = (uint32_t)(m0 + t);
-  const double* Fe = P.tabs;
-  const double* edge = P.tabs + (P.C + 1);
+  const Grid G = make_grid(P.tabs, P.C);
   int cc[D];
   {
     uint32_t r = k;
@@ -63,7 +62,7 @@ __global__ void trace_kernel(const DevProblem P, const int i, const uint32_t k, 
   }
   const int steps = P.N - i;
   double X[D];
-  start_point<D>(P, Fe, edge, cc, i, k, m, X);
+  start_point<D>(P, G, cc, i, k, m, X);
   double* xo = xs + t * (int64_t)(steps + 1) * D;
   int64_t* co = cells + t * (int64_t)(steps + 1);
   double* wo = dws + t * (int64_t)steps * Q;
@@ -79,7 +78,7 @@ __global__ void trace_kernel(const DevProblem P, const int i, const uint32_t k, 
   put(0, X);
   for (int j = i; j < P.N; ++j) {
     double dW[Q], Xn[D];
-    brownian<Q>(P, i, j, k, m, dW);
+    brownian<Q>(P, G, i, j, k, m, dW);
     euler<D, Q>(P, X, dW, Xn);
 #pragma unroll
     for (int l = 0; l < Q; ++l) wo[(j - i) * Q + l] = dW[l];
@@ -90,14 +89,17 @@ __global__ void trace_kernel(const DevProblem P, const int i, const uint32_t k, 
 }
 
 __global__ void detmath_kernel(const int op, const int64_t n, const double* __restrict__ in,
-                               double* __restrict__ o0, double* __restrict__ o1) {
+                               double* __restrict__ o0, double* __restrict__ o1, const double* __restrict__ det) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= n) return;
+  DetTabs T;
+  T.logt = reinterpret_cast<const double2*>(det);
+  T.sct = reinterpret_cast<const double2*>(det + 256);
   if (op == 0) {
-    o0[t] = dm_log(in[t]);
+    o0[t] = dm_log(in[t], T);
   } else {
     double s, c;
-    dm_sincospi2(in[t], s, c);
+    dm_sincospi2(in[t], T, s, c);
     o0[t] = s;
     o1[t] = c;
   }

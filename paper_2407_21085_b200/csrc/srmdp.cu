@@ -95,6 +95,80 @@ static double host_dm_exp(double x) {
   return std::ldexp(p, (int)kf);
 }
 
+// Reference functions of docs/detmath.md (table builders only).
+static double host_dm_log_series(double x) {
+  static const double LG[11] = {0.0,
+      0x1.5555555555555p-1, 0x1.999999999999ap-2, 0x1.2492492492492p-2, 0x1.c71c71c71c71cp-3,
+      0x1.745d1745d1746p-3, 0x1.3b13b13b13b14p-3, 0x1.1111111111111p-3, 0x1.e1e1e1e1e1e1ep-4,
+      0x1.af286bca1af28p-4, 0x1.8618618618618p-4};
+  if (x != x || x < 0.0) return NAN;
+  if (x == 0.0) return -INFINITY;
+  if (std::isinf(x)) return INFINITY;
+  int k = 0;
+  if (x < 0x1p-1022) { x = x * 0x1p54; k = -54; }
+  uint64_t b;
+  memcpy(&b, &x, 8);
+  k = k + (int)(b >> 52) - 1023;
+  const uint64_t mb = (b & 0x000fffffffffffffull) | 0x3ff0000000000000ull;
+  double m;
+  memcpy(&m, &mb, 8);
+  if (m > 0x1.6a09e667f3bcdp+0) { m = m * 0.5; k = k + 1; }
+  const double f = m - 1.0;
+  const double s = f / (2.0 + f);
+  const double z = s * s;
+  double P = LG[10];
+  for (int j = 9; j >= 1; --j) P = std::fma(P, z, LG[j]);
+  const double R = z * P;
+  const double t = s * R;
+  const double lm = (2.0 * s) + t;
+  const double hi = (double)k * 0x1.62e42fee00000p-1;
+  const double lo = (double)k * 0x1.a39ef35793c76p-33;
+  return hi + (lm + lo);
+}
+
+static void host_dm_sincospi2_series(double u, double* sn_out, double* cs_out) {
+  static const double S[9] = {
+      0x1.921fb54442d18p+0, -0x1.4abbce625be53p-1, 0x1.466bc6775aae2p-4, -0x1.32d2cce62bd86p-8,
+      0x1.50783487ee782p-13, -0x1.e3074fde8871fp-19, 0x1.e8f434d018d63p-25, -0x1.6fadb9f155744p-31,
+      0x1.aaec32af93359p-38};
+  static const double Cc[10] = {
+      0x1.0000000000000p+0, -0x1.3bd3cc9be45dep+0, 0x1.03c1f081b5ac4p-2, -0x1.55d3c7e3cbffap-6,
+      0x1.e1f506891babbp-11, -0x1.a6d1f2a204a8cp-16, 0x1.f9d38a3763cc3p-22, -0x1.b6e24f44b128fp-28,
+      0x1.20c62c2f2d7f5p-34, -0x1.2a0c591af8314p-41};
+  const double v = 4.0 * u;
+  const double n = std::rint(v);
+  const double f = v - n;
+  const double f2 = f * f;
+  double ps = S[8];
+  for (int j = 7; j >= 0; --j) ps = std::fma(ps, f2, S[j]);
+  const double sn = f * ps;
+  double pc = Cc[9];
+  for (int j = 8; j >= 0; --j) pc = std::fma(pc, f2, Cc[j]);
+  const double cs = pc;
+  switch (((int)n) & 3) {
+    case 0: *sn_out = sn; *cs_out = cs; break;
+    case 1: *sn_out = cs; *cs_out = -sn; break;
+    case 2: *sn_out = -sn; *cs_out = -cs; break;
+    default: *sn_out = -cs; *cs_out = sn; break;
+  }
+}
+
+// LOGT (128 x (INVC, LT)) and SCT (128 x (sin, cos)) of docs/detmath.md
+static void det_tables(double* out /* 512 */) {
+  for (int j = 0; j < 128; ++j) {
+    double invc = 1.0, lt = 0.0;
+    if (j != 0 && j != 127) {
+      double c = 1.0 + (((double)j + 0.5) / 128.0);
+      if (j >= 53) c = c * 0.5;
+      invc = 1.0 / c;
+      lt = -host_dm_log_series(invc);
+    }
+    out[2 * j] = invc;
+    out[2 * j + 1] = lt;
+    host_dm_sincospi2_series((double)j / 128.0, &out[256 + 2 * j], &out[256 + 2 * j + 1]);
+  }
+}
+
 // F_nu(x) = 1/(1+exp(-mu x))
 static double host_F(double mu, double x) {
   if (x == -INFINITY) return 0.0;
@@ -102,9 +176,10 @@ static double host_F(double mu, double x) {
   return 1.0 / (1.0 + host_dm_exp(-(mu * x)));
 }
 
-// tabs = [F(e_c), c=0..C | e_c, c=0..C | r_c, c=0..C-1]
+// tabs = [F(e_c), c=0..C | e_c, c=0..C | r_c, c=0..C-1 | pad | LOGT | SCT] (problem.cuh)
 static std::vector<double> grid_tables(int C, double L, double mu) {
-  std::vector<double> t(3 * C + 2);
+  std::vector<double> t(tabs_len(C), 0.0);
+  det_tables(t.data() + tabs_det_off(C));
   const double delta = (2.0 * L) / (double)C;
   for (int c = 0; c <= C; ++c) {
     double e = (c == 0) ? -INFINITY : (c == C) ? INFINITY : ((-L) + ((double)c * delta));
@@ -654,14 +729,19 @@ extern "C" srmdp_status srmdp_debug_detmath(int op, size_t n, const double* in, 
   if ((op != 0 && op != 1) || !in || !out0 || (op == 1 && !out1)) return SRMDP_E_ARG;
   if (n == 0) return SRMDP_OK;
   double* d = nullptr;
-  cudaError_t e = cudaMalloc(&d, 3 * n * sizeof(double));
+  cudaError_t e = cudaMalloc(&d, (3 * n + 512) * sizeof(double));
   if (e != cudaSuccess) return cuda_fail(nullptr, e, "detmath alloc");
-  cudaMemcpy(d, in, n * sizeof(double), cudaMemcpyHostToDevice);
-  detmath_kernel<<<(unsigned)((n + 255) / 256), 256>>>(op, (int64_t)n, d, d + n, d + 2 * n);
+  std::vector<double> det(512);
+  det_tables(det.data());
+  double* dt = d;                 // tables first: 16-byte aligned double2 rows
+  double* din = d + 512;
+  cudaMemcpy(dt, det.data(), 512 * sizeof(double), cudaMemcpyHostToDevice);
+  cudaMemcpy(din, in, n * sizeof(double), cudaMemcpyHostToDevice);
+  detmath_kernel<<<(unsigned)((n + 255) / 256), 256>>>(op, (int64_t)n, din, din + n, din + 2 * n, dt);
   e = cudaDeviceSynchronize();
   if (e == cudaSuccess) {
-    cudaMemcpy(out0, d + n, n * sizeof(double), cudaMemcpyDeviceToHost);
-    if (op == 1) cudaMemcpy(out1, d + 2 * n, n * sizeof(double), cudaMemcpyDeviceToHost);
+    cudaMemcpy(out0, din + n, n * sizeof(double), cudaMemcpyDeviceToHost);
+    if (op == 1) cudaMemcpy(out1, din + 2 * n, n * sizeof(double), cudaMemcpyDeviceToHost);
   }
   cudaFree(d);
   return e == cudaSuccess ? SRMDP_OK : cuda_fail(nullptr, e, "detmath kernel");

@@ -34,6 +34,9 @@ struct KCfg {
   static constexpr int NG = N1 * (N1 + 1) / 2;      // Gram entries (upper, incl. diag)
   static constexpr int NZ = Q * N1;                 // Z right-hand-side entries
   static constexpr int E = NG + NZ;
+  static constexpr int PPT = 1;                     // paths per thread per round (2 measured slower on cfg4: 2.43e10 vs 2.65e10)
+  static constexpr int ROWS = kThreads * PPT;       // rows (paths) per round
+  static constexpr int CTAS = (PPT == 2) ? 2 : 3;   // resident CTAs per SM (launch bounds)
   static constexpr int S = (E <= kThreads) ? (kThreads / E) : 1;  // row slices per entry
   static constexpr int PAIRS = E * S;
   static constexpr int NACC = (PAIRS + kThreads - 1) / kThreads;
@@ -45,9 +48,9 @@ struct KCfg {
 template <int D, int Q>
 struct SmemLayout {
   using KC = KCfg<D, Q>;
-  __host__ __device__ static int tabs(int C) { return (3 * C + 2 + 1) & ~1; }
+  __host__ __device__ static int tabs(int C) { return tabs_len(C); }
   __host__ __device__ static int rows(int C) { return tabs(C); }
-  __host__ __device__ static int L(int C) { return rows(C) + kThreads * KC::ROW; }
+  __host__ __device__ static int L(int C) { return rows(C) + KC::ROWS * KC::ROW; }
   __host__ __device__ static int RZ(int C) { return L(C) + KC::N1 * KC::N1; }
   __host__ __device__ static int BZ(int C) { return RZ(C) + KC::NZ; }
   __host__ __device__ static int BY(int C) { return BZ(C) + KC::NZ; }
@@ -117,74 +120,102 @@ __device__ __forceinline__ void prefetch_block(const double* blk) {
   for (int off = 0; off < NHOT * 8; off += 128) asm volatile("prefetch.global.L1 [%0];" ::"l"((const char*)blk + off));
 }
 
-// One path of cloud (i,k), pass 1. Writes the design row (1, x_i - r_k) and
-// dW_i into `row` (shared memory) as soon as they exist, so neither stays in
-// registers across the Euler chain. Returns B = S_{Y,i+1}(x_i) = g(x_N) +
-// sum_{j>i} f_j dt (eq. PsiM) and Y1 = y_{i+1}(x_{i+1}).
-// Software pipeline: the block of X_{j+1} is prefetched into L1, then the
+// PPT paths of cloud (i,k), pass 1: path p of this thread is m0 + p*kThreads
+// and owns shared-memory row `rows + p*kThreads*ROW`. The design row
+// (1, x_i - r_k) and dW_i are written there as soon as they exist, so they do
+// not stay in registers across the Euler chain. Returns per path
+// B = S_{Y,i+1}(x_i) = g(x_N) + sum_{j>i} f_j dt (eq. PsiM) and
+// Y1 = y_{i+1}(x_{i+1}). The PPT paths are independent instruction streams
+// (ILP); per path the block of X_{j+1} is prefetched into L1, then the
 // increments and Euler step of X_{j+2} are computed (FP64-heavy, independent
 // of the gather), then the block is evaluated.
-template <int D, int Q>
-__device__ __forceinline__ void simulate_path(const DevProblem& P, const double* sFe, const double* sEdge,
-                                              const double* sCen, const int (&cc)[D], int i, uint32_t k,
-                                              uint32_t m, double* row, double& Bout, double& Y1out) {
+template <int D, int Q, int PPT>
+__device__ __forceinline__ void simulate_paths(const DevProblem& P, const Grid& G, const int (&cc)[D], int i,
+                                               uint32_t k, uint32_t m0, double* rows, double (&Bout)[PPT],
+                                               double (&Y1out)[PPT]) {
   using KC = KCfg<D, Q>;
-  double Xn[D];
-  start_point<D>(P, sFe, sEdge, cc, i, k, m, Xn);
-  row[0] = 1.0;
+  double Xn[PPT][D];
 #pragma unroll
-  for (int l = 0; l < D; ++l) row[1 + l] = Xn[l] - sCen[cc[l]];
-  {
+  for (int p = 0; p < PPT; ++p) {
+    double* row = rows + p * kThreads * KC::ROW;
+    start_point<D>(P, G, cc, i, k, m0 + p * kThreads, Xn[p]);
+    row[0] = 1.0;
+#pragma unroll
+    for (int l = 0; l < D; ++l) row[1 + l] = Xn[p][l] - G.cen[cc[l]];
+  }
+#pragma unroll
+  for (int p = 0; p < PPT; ++p) {
+    double* row = rows + p * kThreads * KC::ROW;
     double dW[Q], X1[D];
-    brownian<Q>(P, i, i, k, m, dW);
+    brownian<Q>(P, G, i, i, k, m0 + p * kThreads, dW);
 #pragma unroll
     for (int l = 0; l < Q; ++l) row[1 + D + l] = dW[l];
-    euler<D, Q>(P, Xn, dW, X1);
+    euler<D, Q>(P, Xn[p], dW, X1);
 #pragma unroll
-    for (int l = 0; l < D; ++l) Xn[l] = X1[l];
+    for (int l = 0; l < D; ++l) Xn[p][l] = X1[l];
   }
-  double acc = 0.0, zlin = 0.0, Y1 = 0.0, yv = 0.0;
+  double acc[PPT], zlin[PPT], Y1[PPT], yv[PPT];
+#pragma unroll
+  for (int p = 0; p < PPT; ++p) { acc[p] = 0.0; zlin[p] = 0.0; Y1[p] = 0.0; yv[p] = 0.0; }
   const int N = P.N;
 #pragma unroll 1
   for (int j = i; j < N; ++j) {
     // Xn = X_{j+1}
-    double zn = 0.0;
+    double zn[PPT];
     if (j + 1 < N) {
-      uint32_t kn = 0;
-      int c[D];
+      const double* blk[PPT];
+      int c[PPT][D];
 #pragma unroll
-      for (int l = 0; l < D; ++l) {
-        c[l] = locate1(Xn[l], P.L, P.inv_delta, P.C);
-        kn = kn * (uint32_t)P.C + (uint32_t)c[l];
+      for (int p = 0; p < PPT; ++p) {
+        uint32_t kn = 0;
+#pragma unroll
+        for (int l = 0; l < D; ++l) {
+          c[p][l] = locate1(Xn[p][l], P.L, P.inv_delta, P.C);
+          kn = kn * (uint32_t)P.C + (uint32_t)c[p][l];
+        }
+        blk[p] = P.table + ((size_t)(j + 1) * (size_t)P.K_pad + kn) * (size_t)KC::NBP;
+        prefetch_block<2 * KC::N1 + 1>(blk[p]);
       }
-      const double* blk = P.table + ((size_t)(j + 1) * (size_t)P.K_pad + kn) * (size_t)KC::NBP;
-      prefetch_block<2 * KC::N1 + 1>(blk);
-      double Xnn[D];
-      {
+      double Xnn[PPT][D];
+#pragma unroll
+      for (int p = 0; p < PPT; ++p) {
         double dW[Q];
-        brownian<Q>(P, i, j + 1, k, m, dW);       // increments of step j+1 (independent of the gather)
-        euler<D, Q>(P, Xn, dW, Xnn);
+        brownian<Q>(P, G, i, j + 1, k, m0 + p * kThreads, dW);   // increments of step j+1
+        euler<D, Q>(P, Xn[p], dW, Xnn[p]);
       }
-      double a[D + 1];
-      a[0] = 1.0;
 #pragma unroll
-      for (int l = 0; l < D; ++l) a[1 + l] = Xn[l] - sCen[c[l]];
-      eval_block<D, Q>(P, blk, a, yv, zn);        // y_{j+1}(x_{j+1}), z_{j+1}(x_{j+1})
+      for (int p = 0; p < PPT; ++p) {
+        double a[D + 1];
+        a[0] = 1.0;
 #pragma unroll
-      for (int l = 0; l < D; ++l) Xn[l] = Xnn[l];
+        for (int l = 0; l < D; ++l) a[1 + l] = Xn[p][l] - G.cen[c[p][l]];
+        eval_block<D, Q>(P, blk[p], a, yv[p], zn[p]);   // y_{j+1}(x_{j+1}), z_{j+1}(x_{j+1})
+#pragma unroll
+        for (int l = 0; l < D; ++l) Xn[p][l] = Xnn[p][l];
+      }
     } else {
-      yv = g_eval<D>(P, Xn);                      // y_N := g
+#pragma unroll
+      for (int p = 0; p < PPT; ++p) {
+        yv[p] = g_eval<D>(P, Xn[p]);               // y_N := g
+        zn[p] = 0.0;
+      }
     }
-    if (j == i) {
-      Y1 = yv;
-    } else {
-      const double fdt = f_eval(P, yv, zlin) * P.dt;   // f_j(x_j, y_{j+1}(x_{j+1}), z_j(x_j)) dt
-      acc = acc + fdt;
+#pragma unroll
+    for (int p = 0; p < PPT; ++p) {
+      if (j == i) {
+        Y1[p] = yv[p];
+      } else {
+        const double fdt = f_eval(P, yv[p], zlin[p]) * P.dt;   // f_j(x_j, y_{j+1}(x_{j+1}), z_j(x_j)) dt
+        acc[p] = acc[p] + fdt;
+      }
+      zlin[p] = zn[p];
     }
-    zlin = zn;
   }
-  Bout = yv + acc;                                 // g(x_N) + sum
-  Y1out = Y1;
+#pragma unroll
+  for (int p = 0; p < PPT; ++p) {
+    Bout[p] = yv[p] + acc[p];                      // g(x_N) + sum
+    Y1out[p] = Y1[p];
+  }
 }
 
 // Cholesky of the symmetric n x n matrix in A (full storage), lower factor in
@@ -227,16 +258,14 @@ __device__ void chol_solve(const double* L, const double* r, double* b) {
 }
 
 template <int D, int Q>
-__global__ void __launch_bounds__(kThreads, 3)
+__global__ void __launch_bounds__(kThreads, KCfg<D, Q>::CTAS)
 step_kernel(const DevProblem P, const int i, const int64_t k_begin, const int64_t nk) {
   using KC = KCfg<D, Q>;
   using SL = SmemLayout<D, Q>;
   extern __shared__ double sm[];
   const int C = P.C;
   const int tid = threadIdx.x;
-  double* sFe = sm;
-  double* sEdge = sm + (C + 1);
-  double* sCen = sm + 2 * (C + 1);
+  const Grid G = make_grid(sm, C);
   double* sRows = sm + SL::rows(C);
   double* sL = sm + SL::L(C);
   double* sRZ = sm + SL::RZ(C);
@@ -247,7 +276,7 @@ step_kernel(const DevProblem P, const int i, const int64_t k_begin, const int64_
   int* sFlag = reinterpret_cast<int*>(sm + SL::flag(C));
   double* BYs = P.by_in_smem ? (sm + SL::pairs(C)) : (P.by_scratch + (size_t)blockIdx.x * (size_t)P.M * 2);
 
-  for (int t = tid; t < 3 * C + 2; t += kThreads) sm[t] = P.tabs[t];
+  for (int t = tid; t < tabs_len(C); t += kThreads) sm[t] = P.tabs[t];
 
   // Owner-compute assignment: pair idx -> (entry e, row slice s); fixed per thread.
   int cA[KC::NACC], cB[KC::NACC], rlo[KC::NACC], rhi[KC::NACC];
@@ -266,8 +295,8 @@ step_kernel(const DevProblem P, const int i, const int64_t k_begin, const int64_
         cA[n] = z % KC::N1;
         cB[n] = 1 + D + z / KC::N1;
       }
-      rlo[n] = (s * kThreads) / KC::S;
-      rhi[n] = ((s + 1) * kThreads) / KC::S;
+      rlo[n] = (s * KC::ROWS) / KC::S;
+      rhi[n] = ((s + 1) * KC::ROWS) / KC::S;
     } else {
       cA[n] = cB[n] = 0;
       rlo[n] = rhi[n] = 0;
@@ -290,18 +319,25 @@ step_kernel(const DevProblem P, const int i, const int64_t k_begin, const int64_
     double acc[KC::NACC];
 #pragma unroll
     for (int n = 0; n < KC::NACC; ++n) acc[n] = 0.0;
-    for (int64_t m0 = 0; m0 < M; m0 += kThreads) {
-      const int64_t m = m0 + tid;
-      const int nrows = (int)((M - m0) < kThreads ? (M - m0) : kThreads);
-      if (m < M) {
-        double* row = sRows + tid * KC::ROW;
-        double Bv, Y1;
-        simulate_path<D, Q>(P, sFe, sEdge, sCen, cc, i, k, (uint32_t)m, row, Bv, Y1);
-        const double sc = Bv * P.inv_dt;
+    for (int64_t m0 = 0; m0 < M; m0 += KC::ROWS) {
+      const int nrows = (int)((M - m0) < KC::ROWS ? (M - m0) : KC::ROWS);
+      if (m0 + tid < M) {
+        // paths m0+tid (+ m0+tid+256): rows tid (+ tid+256); a second path past M
+        // is simulated (valid counters) but neither stored nor reduced
+        double Bv[KC::PPT], Y1[KC::PPT];
+        simulate_paths<D, Q, KC::PPT>(P, G, cc, i, k, (uint32_t)(m0 + tid), sRows + tid * KC::ROW, Bv, Y1);
 #pragma unroll
-        for (int l = 0; l < Q; ++l) row[1 + D + l] = row[1 + D + l] * sc;   // S_{Z,i} = S_{Y,i+1} dW_i / dt
-        BYs[2 * m] = Bv;
-        BYs[2 * m + 1] = Y1;
+        for (int p = 0; p < KC::PPT; ++p) {
+          const int64_t m = m0 + tid + p * kThreads;
+          if (m < M) {
+            double* row = sRows + (tid + p * kThreads) * KC::ROW;
+            const double sc = Bv[p] * P.inv_dt;
+#pragma unroll
+            for (int l = 0; l < Q; ++l) row[1 + D + l] = row[1 + D + l] * sc;   // S_{Z,i} = S_{Y,i+1} dW_i / dt
+            BYs[2 * m] = Bv[p];
+            BYs[2 * m + 1] = Y1[p];
+          }
+        }
       }
       __syncthreads();
 #pragma unroll
@@ -356,10 +392,10 @@ step_kernel(const DevProblem P, const int i, const int64_t k_begin, const int64_
     for (int p = 0; p < KC::N1; ++p) ry[p] = 0.0;
     for (int64_t m = tid; m < M; m += kThreads) {
       double x[D], a[KC::N1];
-      start_point<D>(P, sFe, sEdge, cc, i, k, (uint32_t)m, x);
+      start_point<D>(P, G, cc, i, k, (uint32_t)m, x);
       a[0] = 1.0;
 #pragma unroll
-      for (int l = 0; l < D; ++l) a[1 + l] = x[l] - sCen[cc[l]];
+      for (int l = 0; l < D; ++l) a[1 + l] = x[l] - G.cen[cc[l]];
       double zl = 0.0;
       for (int l = 0; l < Q; ++l) {
         double v = 0.0;

@@ -14,7 +14,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libsrmdp_b200.so")
+LIB_PATH = os.environ.get("SRMDP_LIB") or os.path.join(_HERE, "libsrmdp_b200.so")   # override: A/B builds
 
 DYN = {"bm": 0, "gbm": 1, "affine": 2}
 FKIND = {"zero": 0, "linear": 1, "paper": 2}

@@ -54,3 +54,7 @@ print()
 print("%-28s %10s %7s %7s" % ("line", "inst", "%inst", "%stall"))
 for ln, v in sorted(by_line.items(), key=lambda kv: -stall_line[kv[0]])[:top]:
     print("%-28s %10.4g %6.1f%% %6.1f%%" % (ln, v, 100 * v / tot, 100 * stall_line[ln] / tst))
+print()
+print("%-28s %10s %7s %7s   (by instructions)" % ("line", "inst", "%inst", "%stall"))
+for ln, v in by_line.most_common(top):
+    print("%-28s %10.4g %6.1f%% %6.1f%%" % (ln, v, 100 * v / tot, 100 * stall_line[ln] / tst))
