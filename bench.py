@@ -35,24 +35,29 @@ import workloads  # noqa: E402
 
 
 # ----------------------------------------------------------------------------
-# algorithmic FP64 work per unit (counts follow the
-# operation sequences of docs/streams.md and docs/detmath.md; fma = 2 flops,
-# add/mul/div/sqrt = 1)
+# algorithmic FP64 work per unit: the per-unit model of SURVEY.md §8(d)
+# (DESIGN.md §5): per path-step q normals at F_norm = 33 flop, the Euler step,
+# locate + centering (3d), the evaluation of y and the q components of z
+# (2(q+1)(d+1)) and the driver; per path-start the inverse CDFs (31 d), Gram,
+# Z / Y right-hand sides, the pass-2 z_i and g. It is the method's work, not
+# the kernel's executed instruction count (the kernel evaluates sum_l w_l z_l
+# through a certified contraction and fewer flops; ncu FP64-pipe utilisation
+# is reported separately in profiles/).
 # ----------------------------------------------------------------------------
-F_PAIR = 77          # one Box-Muller pair: 2 u01 + dm_log 31 + (-2*, sqrt) 2 + dm_sincospi2 38 + scaling 4
-F_COORD = 38         # one conditional-logistic coordinate: u01 1 + inverse CDF 6 + dm_log 31
+F_NORM = 33
 
 
 def flops_per_path_step(w):
     d, q = w["d"], w["q"]
-    euler = {"bm": d, "gbm": 5 * d, "affine": d * (2 * d + 2 * q + 2)}[w["dyn"]]
-    return F_PAIR * math.ceil(q / 2) + euler + 3 * d + 2 * (q + 1) * (d + 1) + 2 * q + 4
+    euler = {"bm": d, "gbm": 4 * d, "affine": d * (2 * d + 2 * q + 2)}[w["dyn"]]
+    f_f = {"zero": 0, "linear": q + 3, "paper": q + 4}[w["f"]]
+    return q * F_NORM + euler + 3 * d + 2 * (q + 1) * (d + 1) + f_f + 2
 
 
 def flops_per_path_start(w):
     d, q = w["d"], w["q"]
-    return (F_COORD * d + d + 2 * q + (d + 1) * (d + 2) + 2 * q * (d + 1)
-            + 2 * q * (d + 1) + 2 * q + 4 + 2 * (d + 1) + (d + 3))
+    f_g = d + 3
+    return 31 * d + (d + 1) * (d + 2) + 4 * q * (d + 1) + 2 * (d + 1) + 3 * q + f_g
 
 
 def algorithmic_flops(w):
