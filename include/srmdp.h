@@ -72,6 +72,11 @@ typedef struct {
 /* Flags */
 #define SRMDP_FLAG_NO_GRAPH     1 /* launch step kernels directly instead of replaying a CUDA graph */
 #define SRMDP_FLAG_TIME_KERNELS 2 /* record CUDA events around every step kernel (srmdp_stats.kernel_ms) */
+#define SRMDP_FLAG_FORCE_NCCL   4 /* use the NCCL exchange even for world == 1 (tests the collective path
+                                     on one GPU; needs nccl_unique_id) */
+#define SRMDP_FLAG_LOOPBACK     8 /* emulate `world` ranks in this process: each step launches the world
+                                     shards one after another on the same table, no NCCL (tests sharding
+                                     and padding on one GPU; `rank` is ignored) */
 
 typedef struct {
   int d, q, N;          /* state dim, Brownian dim, time steps */

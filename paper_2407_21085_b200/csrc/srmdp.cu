@@ -278,6 +278,7 @@ struct srmdp {
   cudaGraphExec_t graph = nullptr;
   ncclComm_t comm = nullptr;
   bool solved = false;
+  int launches_per_solve = 0;
   std::vector<cudaEvent_t> ev;
   srmdp_stats_t st{};
   mutable std::string err = "no error";
@@ -326,7 +327,10 @@ static srmdp_status validate(const srmdp_config* c, std::string& err) {
   if (!(c->mu > 0)) return bad(SRMDP_E_ARG, "mu must be > 0");
   if (c->M < c->d + 1) return bad(SRMDP_E_PRECOND, "M < d+1: the LP1 OLS needs M >= d+1 (P:312)");
   if (c->world < 1 || c->rank < 0 || c->rank >= c->world) return bad(SRMDP_E_ARG, "bad rank/world");
-  if (c->world > 1 && !c->nccl_unique_id) return bad(SRMDP_E_ARG, "world > 1 needs nccl_unique_id");
+  const bool loopback = c->flags & SRMDP_FLAG_LOOPBACK;
+  if (((c->world > 1 && !loopback) || (c->flags & SRMDP_FLAG_FORCE_NCCL)) && !c->nccl_unique_id)
+    return bad(SRMDP_E_ARG, "the NCCL exchange needs nccl_unique_id");
+  if (loopback && (c->flags & SRMDP_FLAG_FORCE_NCCL)) return bad(SRMDP_E_ARG, "LOOPBACK and FORCE_NCCL exclude each other");
   if (c->dyn.kind < 0 || c->dyn.kind > 2 || c->driver.kind < 0 || c->driver.kind > 2 || c->terminal.kind < 0 ||
       c->terminal.kind > 1)
     return bad(SRMDP_E_ARG, "unknown problem family kind");
@@ -373,12 +377,26 @@ static srmdp_status enqueue_sweep(srmdp_t* h) {
   const bool timed = h->cfg.flags & SRMDP_FLAG_TIME_KERNELS;
   CK(h, cudaMemsetAsync(h->d_lp0, 0, sizeof(unsigned long long), h->stream), "memset");
   const int64_t nk = h->k_end - h->k_begin;
+  const bool loopback = h->cfg.flags & SRMDP_FLAG_LOOPBACK;
+  h->launches_per_solve = 0;
   for (int i = h->N - 1; i >= 0; --i) {
     if (timed) CK(h, record_event(h, h->ev[2 * i]), "event");
-    if (nk > 0) h->ops->step(h->dp, i, h->k_begin, nk, h->grid, h->smem, h->stream);
+    if (loopback) {
+      for (int r = 0; r < h->cfg.world; ++r) {   // shards in sequence on one table
+        int64_t plan[4];
+        srmdp_shard_plan(h->K, h->cfg.world, r, plan);
+        if (plan[1] > plan[0]) {
+          h->ops->step(h->dp, i, plan[0], plan[1] - plan[0], h->grid, h->smem, h->stream);
+          ++h->launches_per_solve;
+        }
+      }
+    } else if (nk > 0) {
+      h->ops->step(h->dp, i, h->k_begin, nk, h->grid, h->smem, h->stream);
+      ++h->launches_per_solve;
+    }
     CK(h, cudaGetLastError(), "step kernel launch");
     if (timed) CK(h, record_event(h, h->ev[2 * i + 1]), "event");
-    if (h->cfg.world > 1) {
+    if (h->comm) {
       double* slice = h->d_table + (size_t)i * h->K_pad * h->B_pad;
       const size_t cnt = (size_t)h->chunk * h->B_pad;
       ncclResult_t r = nccl().AllGather(slice + (size_t)h->cfg.rank * cnt, slice, cnt, ncclDouble, h->comm, h->stream);
@@ -405,8 +423,9 @@ extern "C" srmdp_status srmdp_create(const srmdp_config* cfg, srmdp_t** out) {
   h->B = (h->q + 1) * (h->d + 1);
   h->B_pad = block_stride(h->d, h->q);
   int64_t plan[4];
-  srmdp_shard_plan(h->K, cfg->world, cfg->rank, plan);
+  srmdp_shard_plan(h->K, cfg->world, (cfg->flags & SRMDP_FLAG_LOOPBACK) ? 0 : cfg->rank, plan);
   h->k_begin = plan[0]; h->k_end = plan[1]; h->chunk = plan[2]; h->K_pad = plan[3];
+  if (cfg->flags & SRMDP_FLAG_LOOPBACK) { h->k_begin = 0; h->k_end = h->K; }
   h->ops = find_ops(h->d, h->q);
   // truncation constants: override, else eq. prop:bound (reading R5)
   double by, bz;
@@ -465,7 +484,7 @@ extern "C" srmdp_status srmdp_create(const srmdp_config* cfg, srmdp_t** out) {
     else cuda_fail(h, e, "kernel attributes");
     return fail(SRMDP_E_UNSUPPORTED);
   }
-  const int64_t nk = h->k_end - h->k_begin;
+  const int64_t nk = (cfg->flags & SRMDP_FLAG_LOOPBACK) ? h->chunk : h->k_end - h->k_begin;
   const int64_t full = (int64_t)h->ctas * h->sms;
   h->grid = (int)(nk < full ? (nk > 0 ? nk : 1) : full);
   if (!by_smem) {
@@ -511,7 +530,7 @@ extern "C" srmdp_status srmdp_create(const srmdp_config* cfg, srmdp_t** out) {
     h->ev.resize(2 * h->N);
     for (auto& x : h->ev) cudaEventCreate(&x);
   }
-  if (cfg->world > 1) {
+  if ((cfg->world > 1 && !(cfg->flags & SRMDP_FLAG_LOOPBACK)) || (cfg->flags & SRMDP_FLAG_FORCE_NCCL)) {
     NcclApi& api = nccl();
     if (!api.ok) { h->err = api.err; return fail(SRMDP_E_NCCL); }
     ncclUniqueId id;
@@ -551,7 +570,7 @@ extern "C" srmdp_status srmdp_solve(srmdp_t* h) {
   unsigned long long lp0 = 0;
   CK(h, cudaMemcpy(&lp0, h->d_lp0, sizeof(lp0), cudaMemcpyDeviceToHost), "lp0 count");
   h->st.lp0_fallbacks = lp0;
-  h->st.kernel_launches = (h->k_end > h->k_begin) ? h->N : 0;
+  h->st.kernel_launches = h->launches_per_solve;
   if (h->cfg.flags & SRMDP_FLAG_TIME_KERNELS) {
     double tot = 0;
     for (int i = 0; i < h->N; ++i) {

@@ -36,7 +36,9 @@ struct KCfg {
   static constexpr int E = NG + NZ;
   static constexpr int PPT = 1;                     // paths per thread per round (2 measured slower on cfg4: 2.43e10 vs 2.65e10)
   static constexpr int ROWS = kThreads * PPT;       // rows (paths) per round
-  static constexpr int CTAS = (PPT == 2) ? 2 : 3;   // resident CTAs per SM (launch bounds)
+  // resident CTAs per SM (launch bounds): 3 (<= 85 registers) up to d = 8; the
+  // high-d kernels keep their d-long state in 128 registers at 2 CTAs/SM
+  static constexpr int CTAS = (PPT == 2 || D > 8) ? 2 : 3;
   static constexpr int S = (E <= kThreads) ? (kThreads / E) : 1;  // row slices per entry
   static constexpr int PAIRS = E * S;
   static constexpr int NACC = (PAIRS + kThreads - 1) / kThreads;

@@ -21,6 +21,8 @@ FKIND = {"zero": 0, "linear": 1, "paper": 2}
 GKIND = {"affine": 0, "paper": 1}
 FLAG_NO_GRAPH = 1
 FLAG_TIME_KERNELS = 2
+FLAG_FORCE_NCCL = 4
+FLAG_LOOPBACK = 8
 
 STATUS = {0: "SRMDP_OK", -1: "SRMDP_E_ARG", -2: "SRMDP_E_PRECOND", -3: "SRMDP_E_STATE", -4: "SRMDP_E_CUDA",
           -5: "SRMDP_E_NCCL", -6: "SRMDP_E_NOMEM", -7: "SRMDP_E_UNSUPPORTED"}
