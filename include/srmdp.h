@@ -95,6 +95,9 @@ typedef struct {
   int device;           /* CUDA device ordinal of this rank */
   void* stream;         /* cudaStream_t to run on; NULL = a library-owned stream */
   int flags;            /* SRMDP_FLAG_* */
+  int lp0;              /* 0: LP1 affine local basis (the hot path); nonzero: LP0
+                           piecewise-constant basis (eq. lp0:explicit P:700-707):
+                           every coefficient block is (mean, 0, ..., 0) */
 } srmdp_config;
 
 /* Validate, compute C_y/C_z, build the per-dimension breakpoint/F tables,
@@ -118,6 +121,11 @@ srmdp_status srmdp_coeffs(const srmdp_t* h, int i, int basis, double* out, size_
  * row-major): y[n] = T_{C_y}(y_i^(M)(x)), z[n x q] = T_{C_z}(z_i^(M)(x)) (may be
  * NULL). i == N gives y = g(x) and requires z == NULL. */
 srmdp_status srmdp_eval(const srmdp_t* h, int i, size_t n, const double* x, double* y, double* z);
+
+/* Replace the Philox key (docs/streams.md §2) for the next srmdp_solve: a new,
+ * independent set of clouds on the same problem (independent runs, e.g. the
+ * MSE indicators of eq. mse). Collective (same seed on all ranks). */
+srmdp_status srmdp_reseed(srmdp_t* h, uint64_t seed);
 
 void srmdp_destroy(srmdp_t* h);
 

@@ -596,15 +596,16 @@ static int64_t step_cell(const or_problem* p, double* table, int i, int64_t k) {
   double* SZ0 = (double*)malloc(sizeof(double) * (size_t)M * q);
   memcpy(SZ0, SZ, sizeof(double) * (size_t)M * q);
   memcpy(A2, A, sizeof(double) * (size_t)M * n);
-  /* Z first: OLS(S_Z, L_Z,k, nu_{i,k,M}). */
-  int ok = or_ols_qr(A2, M, n, SZ, q, betaZ);
+  /* Z first: OLS(S_Z, L_Z,k, nu_{i,k,M}). LP0: the OLS on the
+   * constant basis is the mean (eq. lp0:explicit). */
+  int ok = p->lp0 ? 0 : or_ols_qr(A2, M, n, SZ, q, betaZ);
   if (ok) {
     for (int l = 0; l < q; l++)
       for (int j = 0; j < n; j++) blk[(size_t)(1 + l) * n + j] = betaZ[j * q + l];
   } else {
-    /* Rank-deficient design: LP0 fallback (eq. lp0:explicit P:700-707,
-     * reading R15) = mean of the responses, counted. */
-    fallbacks = 1;
+    /* LP0 basis, or rank-deficient LP1 design: LP0 fallback (eq. lp0:explicit
+     * P:700-707, reading R15) = mean of the responses (fallbacks counted). */
+    fallbacks = p->lp0 ? 0 : 1;
     for (int l = 0; l < q; l++) {
       double s = 0.0;
       for (int64_t m = 0; m < M; m++) s = s + SZ0[m * q + l];

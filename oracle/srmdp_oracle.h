@@ -40,6 +40,7 @@ typedef struct {
   int64_t M;              /* paths per cloud */
   double C_y, C_z;        /* truncation bounds (INFINITY = none) */
   uint64_t seed;          /* Philox key, docs/streams.md */
+  int lp0;                /* LP0 piecewise-constant basis (eq. lp0:explicit P:700-707) */
 } or_problem;
 
 /* --- primitives (docs/streams.md, docs/detmath.md) --- */

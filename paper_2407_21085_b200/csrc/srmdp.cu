@@ -499,6 +499,7 @@ extern "C" srmdp_status srmdp_create(const srmdp_config* cfg, srmdp_t** out) {
   P.dyn = cfg->dyn.kind; P.fk = cfg->driver.kind; P.gk = cfg->terminal.kind;
   P.nbd = (h->d + 1) / 2; P.nbq = (h->q + 1) / 2;
   P.by_in_smem = by_smem ? 1 : 0;
+  P.lp0 = cfg->lp0 ? 1 : 0;
   P.K = h->K; P.K_pad = h->K_pad; P.M = h->M;
   P.T = cfg->T;
   P.dt = cfg->T / (double)h->N;
@@ -666,6 +667,25 @@ extern "C" srmdp_status srmdp_eval(const srmdp_t* h, int i, size_t n, const doub
   CK(h, cudaMemcpyAsync(y, dy, n * sizeof(double), cudaMemcpyDeviceToHost, h->stream), "eval d2h");
   if (z) CK(h, cudaMemcpyAsync(z, dz, nz * sizeof(double), cudaMemcpyDeviceToHost, h->stream), "eval d2h");
   CK(h, cudaStreamSynchronize(h->stream), "eval");
+  return SRMDP_OK;
+}
+
+extern "C" srmdp_status srmdp_reseed(srmdp_t* h, uint64_t seed) {
+  if (!h) return SRMDP_E_ARG;
+  h->cfg.seed = seed;
+  DevProblem& P = h->dp;
+  P.key0 = (uint32_t)(seed & 0xffffffffu);
+  P.key1 = (uint32_t)(seed >> 32);
+  for (int r = 0; r < 10; ++r) {
+    P.rkey.k0[r] = P.key0 + (uint32_t)r * 0x9E3779B9u;
+    P.rkey.k1[r] = P.key1 + (uint32_t)r * 0xBB67AE85u;
+  }
+  if (h->graph) {               // kernel parameters are baked into the graph: re-capture
+    cudaSetDevice(h->cfg.device);
+    cudaGraphExecDestroy(h->graph);
+    h->graph = nullptr;
+  }
+  h->solved = false;
   return SRMDP_OK;
 }
 

@@ -447,7 +447,7 @@ step_kernel(const DevProblem P, const int i, const int64_t k_begin, const int64_
     }
     }
     __syncthreads();
-    if (tid == 0) sFlag[0] = cholesky_inplace<KC::N1>(sL);
+    if (tid == 0) sFlag[0] = P.lp0 ? 0 : cholesky_inplace<KC::N1>(sL);   // LP0: means below
     __syncthreads();
     const int ok = sFlag[0];
     // ---------------- solve Z ---------------------------------
@@ -500,9 +500,9 @@ step_kernel(const DevProblem P, const int i, const int64_t k_begin, const int64_
       if (ok) {
         chol_solve<KC::N1>(sL, sRY, sBY);
       } else {
-        sBY[0] = sRY[0] / (double)M;
+        sBY[0] = sRY[0] / (double)M;               // eq. lp0:explicit
         for (int p = 1; p < KC::N1; ++p) sBY[p] = 0.0;
-        atomicAdd(P.lp0_count, 1ull);
+        if (!P.lp0) atomicAdd(P.lp0_count, 1ull);  // rank-deficient LP1 fallback (R15)
       }
     }
     __syncthreads();

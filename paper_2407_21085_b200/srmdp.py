@@ -49,6 +49,7 @@ class srmdp_config(ctypes.Structure):
         ("seed", ctypes.c_uint64),
         ("rank", ctypes.c_int), ("world", ctypes.c_int), ("nccl_unique_id", ctypes.c_void_p),
         ("device", ctypes.c_int), ("stream", ctypes.c_void_p), ("flags", ctypes.c_int),
+        ("lp0", ctypes.c_int),
     ]
 
 
@@ -76,6 +77,7 @@ SIGNATURES = {
     "srmdp_coeffs": (ctypes.c_int, [_H, ctypes.c_int, ctypes.c_int, _PD, ctypes.c_size_t]),
     "srmdp_eval": (ctypes.c_int, [_H, ctypes.c_int, ctypes.c_size_t, _PD, _PD, _PD]),
     "srmdp_destroy": (None, [_H]),
+    "srmdp_reseed": (ctypes.c_int, [_H, ctypes.c_uint64]),
     "srmdp_last_error": (ctypes.c_char_p, [_H]),
     "srmdp_nccl_unique_id": (ctypes.c_int, [ctypes.c_void_p]),
     "srmdp_stats": (ctypes.c_int, [_H, ctypes.POINTER(srmdp_stats_t)]),
@@ -157,6 +159,7 @@ def config_from_workload(w: dict, rank: int = 0, world: int = 1, device: int = 0
     cfg.C_z_override = nan if cz is None else float(cz)
     cfg.seed = int(w["seed"]) & 0xFFFFFFFFFFFFFFFF
     cfg.rank, cfg.world, cfg.device, cfg.flags = rank, world, device, flags
+    cfg.lp0 = 1 if w.get("basis", "lp1") == "lp0" else 0
     if nccl_id is not None:
         idbuf = ctypes.create_string_buffer(bytes(nccl_id), 128)
         keep.append(idbuf)
@@ -202,6 +205,10 @@ def srmdp_eval(h, i: int, x: np.ndarray, d: int, q: int, want_z: bool = True):
     return (y, z) if want_z else y
 
 
+def srmdp_reseed(h, seed: int):
+    _check(library().srmdp_reseed(h, int(seed) & 0xFFFFFFFFFFFFFFFF), h)
+
+
 def srmdp_destroy(h):
     if h:
         library().srmdp_destroy(h)
@@ -218,6 +225,10 @@ class Solver:
 
     def solve(self):
         srmdp_solve(self.h)
+        return self
+
+    def reseed(self, seed):
+        srmdp_reseed(self.h, seed)
         return self
 
     def stats(self):

@@ -41,11 +41,12 @@ def cfg2(seed: int = 1, M: int = 1024, N: int = 10, C: int = 20) -> dict:
                 bs=dict(mu=mu, s=s, r=r, a=1.0, w=[1.0, 1.0]))
 
 
-def benchmark(d: int, N: int, C: int, M: int, seed: int = 1, name: str = "bench") -> dict:
-    """§5.1 benchmark: X=W, d=q, T=1, mu=1, L=6.5, C_g=1, C_f=0."""
+def benchmark(d: int, N: int, C: int, M: int, seed: int = 1, name: str = "bench", basis: str = "lp1") -> dict:
+    """§5.1 benchmark: X=W, d=q, T=1, mu=1, L=6.5, C_g=1, C_f=0.
+    basis "lp1" (affine, the hot path) or "lp0" (piecewise constant)."""
     return dict(name=name, d=d, q=d, N=N, T=1.0, dyn="bm", f="paper", g="paper",
                 C=C, L=6.5, mu=1.0, M=M, C_g=1.0, C_f=0.0, L_f=paper_local_lipschitz(d),
-                seed=seed)
+                seed=seed, basis=basis)
 
 
 def cfg3(seed: int = 1, M: int = 2048) -> dict:
