@@ -230,11 +230,15 @@ def main():
     stream = torch.cuda.current_stream(dev)
     srmdp.library()
 
-    nccl_id = None
-    if world > 1:
+    def fresh_nccl_id():
+        """A new ncclUniqueId per communicator (rank 0 creates, torch.distributed broadcasts)."""
+        if world == 1:
+            return None
         obj = [srmdp.srmdp_nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
-        nccl_id = obj[0]
+        return obj[0]
+
+    nccl_id = fresh_nccl_id()
 
     def barrier():
         torch.cuda.synchronize(dev)
@@ -291,7 +295,8 @@ def main():
     for s in range(1 + args.steps):
         barrier()
         t0 = time.perf_counter()
-        sv = srmdp.Solver(w, rank=rank, world=world, device=local, stream=stream.cuda_stream, nccl_id=nccl_id)
+        sv = srmdp.Solver(w, rank=rank, world=world, device=local, stream=stream.cuda_stream,
+                          nccl_id=fresh_nccl_id())
         sv.solve()
         for i in range(w["N"]):
             sv.coeffs(i, 1, hnp[i])
