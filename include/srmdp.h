@@ -98,6 +98,9 @@ typedef struct {
   int lp0;              /* 0: LP1 affine local basis (the hot path); nonzero: LP0
                            piecewise-constant basis (eq. lp0:explicit P:700-707):
                            every coefficient block is (mean, 0, ..., 0) */
+  int grid;             /* 0: equal-size cells, breakpoints -L + j*2L/#C (default);
+                           1: equal-probability cells under nu, breakpoints F^{-1}(j/#C)
+                           ((A_Strat.) example ii; L unused) */
 } srmdp_config;
 
 /* Validate, compute C_y/C_z, build the per-dimension breakpoint/F tables,

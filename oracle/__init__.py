@@ -52,6 +52,7 @@ class _Problem(ctypes.Structure):
         ("C_y", ctypes.c_double), ("C_z", ctypes.c_double),
         ("seed", ctypes.c_uint64),
         ("lp0", ctypes.c_int),
+        ("grid", ctypes.c_int),
     ]
 
 
@@ -134,7 +135,8 @@ class Problem:
             FKIND[w["f"]], _dptr(self._f) if self._f.size else None,
             GKIND[w["g"]], _dptr(self._g) if self._g.size else None,
             self.C, float(w["L"]), float(w["mu"]), self.M, cy, cz,
-            int(w["seed"]) & 0xFFFFFFFFFFFFFFFF, 1 if w.get("basis", "lp1") == "lp0" else 0)
+            int(w["seed"]) & 0xFFFFFFFFFFFFFFFF, 1 if w.get("basis", "lp1") == "lp0" else 0,
+            1 if w.get("grid", "uniform") == "equiprobable" else 0)
         self.K = int(lib().or_num_cells(ctypes.byref(self.s)))
         self.B = (self.q + 1) * (self.d + 1)
 

@@ -249,6 +249,15 @@ static double edge(int c, int C, double L) {
   return (-L) + ((double)c * delta);
 }
 
+/* Breakpoint c of the problem's grid (docs/streams.md §5/§6b). Equal-probability
+ * strata ((A_Strat.) example ii): e_c = F^{-1}(c/C) = -(1/mu) log(C/c - 1). */
+static double edge_p(const or_problem* p, int c) {
+  if (p->grid == 0) return edge(c, p->C, p->L);
+  if (c <= 0) return -INFINITY;
+  if (c >= p->C) return INFINITY;
+  return (-(1.0 / p->mu)) * or_dm_log(((double)p->C / (double)c) - 1.0);
+}
+
 /* Locate one coordinate: docs/streams.md §6. */
 int or_locate1(double x, int C, double L) {
   double inv_delta = (double)C / (2.0 * L);
@@ -264,9 +273,19 @@ int64_t or_num_cells(const or_problem* p) {
   return K;
 }
 
+/* Cell of one coordinate on the problem's grid: uniform grid as or_locate1;
+ * equal-probability grid: the number of breakpoints e_1..e_{C-1} <= x. */
+static int locate1_p(const or_problem* p, double x) {
+  if (p->grid == 0) return or_locate1(x, p->C, p->L);
+  int c = 0;
+  for (int l = 1; l < p->C; l++)
+    if (x >= edge_p(p, l)) c = l;
+  return c;
+}
+
 int64_t or_locate(const or_problem* p, const double* x) {
   int64_t k = 0;
-  for (int l = 0; l < p->d; l++) k = k * p->C + or_locate1(x[l], p->C, p->L);
+  for (int l = 0; l < p->d; l++) k = k * p->C + locate1_p(p, x[l]);
   return k;
 }
 
@@ -280,6 +299,13 @@ void or_cell_center(const or_problem* p, int64_t k, double* r) {
   int C = p->C;
   double delta = (2.0 * p->L) / (double)C;
   for (int l = 0; l < p->d; l++) {
+    if (p->grid != 0) {   /* equal-probability grid: midpoints, finite edge for outer cells */
+      if (C == 1) r[l] = 0.0;
+      else if (c[l] == 0) r[l] = edge_p(p, 1);
+      else if (c[l] == C - 1) r[l] = edge_p(p, C - 1);
+      else r[l] = (edge_p(p, c[l]) + edge_p(p, c[l] + 1)) * 0.5;
+      continue;
+    }
     if (C == 1) r[l] = 0.0;
     else if (c[l] == 0) r[l] = (-p->L) + (1.0 * delta);
     else if (c[l] == C - 1) r[l] = (-p->L) + ((double)(C - 1) * delta);
@@ -302,13 +328,13 @@ double or_inv_cdf_cond(double mu, double lo, double hi, double U) {
 /* One start-point coordinate in cell c of a dimension, with the membership
  * fix-up of docs/streams.md §5 (reading R7). */
 static double sample_coord(const or_problem* p, int c, double U) {
-  double lo = edge(c, p->C, p->L), hi = edge(c + 1, p->C, p->L);
+  double lo = edge_p(p, c), hi = edge_p(p, c + 1);
   double x = or_inv_cdf_cond(p->mu, lo, hi, U);
   if (isfinite(lo) && x < lo) x = lo;
   if (isfinite(hi) && x >= hi) x = nextafter(hi, -INFINITY);
   int n = 0;
-  while (or_locate1(x, p->C, p->L) < c && n < 4096) { x = nextafter(x, INFINITY); n++; }
-  while (or_locate1(x, p->C, p->L) > c && n < 4096) { x = nextafter(x, -INFINITY); n++; }
+  while (locate1_p(p, x) < c && n < 4096) { x = nextafter(x, INFINITY); n++; }
+  while (locate1_p(p, x) > c && n < 4096) { x = nextafter(x, -INFINITY); n++; }
   return x;
 }
 

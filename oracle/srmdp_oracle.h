@@ -41,6 +41,7 @@ typedef struct {
   double C_y, C_z;        /* truncation bounds (INFINITY = none) */
   uint64_t seed;          /* Philox key, docs/streams.md */
   int lp0;                /* LP0 piecewise-constant basis (eq. lp0:explicit P:700-707) */
+  int grid;               /* 0: equal-size cells on [-L,L]; 1: equal-probability cells under nu */
 } or_problem;
 
 /* --- primitives (docs/streams.md, docs/detmath.md) --- */

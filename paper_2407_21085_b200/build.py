@@ -2,27 +2,39 @@
 
 nvcc for sm_100a only (``-gencode arch=compute_100a,code=sm_100a``), -lineinfo
 for ncu source mapping; the host part is compiled with -ffp-contract=off
-(docs/streams.md). NCCL is loaded at run time (dlopen), only its header is used.
+(docs/streams.md). The per-(d,q) kernel instantiations live in separate
+translation units (csrc/inst_*.cu) compiled in parallel, then linked with the
+host orchestrator (csrc/srmdp.cu). NCCL is loaded at run time (dlopen), only
+its header is used.
 """
 from __future__ import annotations
 
+import glob
 import os
 import subprocess
 import sys
+import tempfile
+from concurrent.futures import ThreadPoolExecutor
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libsrmdp_b200.so")
-SOURCES = [os.path.join(CSRC, f) for f in ("srmdp.cu",)]
-DEPS = SOURCES + [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".h"))] + \
-    [os.path.join(ROOT, "include", f) for f in os.listdir(os.path.join(ROOT, "include"))]
+
+
+def sources():
+    return [os.path.join(CSRC, "srmdp.cu")] + sorted(glob.glob(os.path.join(CSRC, "inst_*.cu")))
+
+
+def deps():
+    return sources() + glob.glob(os.path.join(CSRC, "*.cuh")) + glob.glob(os.path.join(CSRC, "*.h")) + \
+        glob.glob(os.path.join(ROOT, "include", "*.h"))
+
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",
     "-Xcompiler", "-fPIC,-ffp-contract=off,-O2",
-    "-shared",
 ]
 
 
@@ -33,14 +45,36 @@ def nvcc() -> str:
     return "nvcc"
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    stale = force or not os.path.exists(LIB) or max(os.path.getmtime(p) for p in DEPS) > os.path.getmtime(LIB)
+def build(force: bool = False, verbose: bool = False, jobs: int | None = None) -> str:
+    dl = deps()
+    stale = force or not os.path.exists(LIB) or max(os.path.getmtime(p) for p in dl) > os.path.getmtime(LIB)
     if not stale:
         return LIB
+    tmpdir = tempfile.mkdtemp(prefix="srmdp_build_")
+    srcs = sources()
+    objs = [os.path.join(tmpdir, os.path.basename(s) + ".o") for s in srcs]
+    extra = ["-Xptxas", "-v"] if verbose else []
+
+    def compile_one(pair):
+        src, obj = pair
+        r = subprocess.run([nvcc(), *NVCC_FLAGS, *extra, "-c", "-o", obj, src], cwd=CSRC,
+                           capture_output=True, text=True)
+        return src, r
+
+    jobs = jobs or min(len(srcs), os.cpu_count() or 4)
+    with ThreadPoolExecutor(max_workers=jobs) as ex:
+        results = list(ex.map(compile_one, zip(srcs, objs)))
+    for src, r in results:
+        if verbose or r.returncode:
+            sys.stderr.write(r.stdout + r.stderr)
+        if r.returncode:
+            raise RuntimeError("nvcc failed on %s" % src)
     tmp = LIB + ".tmp%d" % os.getpid()
-    cmd = [nvcc(), *NVCC_FLAGS, *(["-Xptxas", "-v"] if verbose else []), "-o", tmp, *SOURCES, "-ldl"]
-    subprocess.check_call(cmd, cwd=CSRC)
+    subprocess.check_call([nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", tmp, *objs, "-ldl"])
     os.replace(tmp, LIB)
+    for o in objs:
+        os.remove(o)
+    os.rmdir(tmpdir)
     return LIB
 
 

@@ -26,7 +26,7 @@ __global__ void eval_kernel(const DevProblem P, const int i, const int64_t n, co
   a[0] = 1.0;
 #pragma unroll
   for (int l = 0; l < D; ++l) {
-    const int c = locate1(x[l], P.L, P.inv_delta, P.C);
+    const int c = P.equi ? locate_g<true>(P, P.tabs + (P.C + 1), x[l]) : locate_g<false>(P, P.tabs + (P.C + 1), x[l]);
     kn = kn * (uint32_t)P.C + (uint32_t)c;
     a[1 + l] = x[l] - __ldg(cen + c);
   }
@@ -62,7 +62,8 @@ __global__ void trace_kernel(const DevProblem P, const int i, const uint32_t k, 
   }
   const int steps = P.N - i;
   double X[D];
-  start_point<D>(P, G, cc, i, k, m, X);
+  if (P.equi) start_point<D, true>(P, G, cc, i, k, m, X);
+  else start_point<D, false>(P, G, cc, i, k, m, X);
   double* xo = xs + t * (int64_t)(steps + 1) * D;
   int64_t* co = cells + t * (int64_t)(steps + 1);
   double* wo = dws + t * (int64_t)steps * Q;
@@ -71,7 +72,7 @@ __global__ void trace_kernel(const DevProblem P, const int i, const uint32_t k, 
 #pragma unroll
     for (int l = 0; l < D; ++l) {
       xo[s * D + l] = v[l];
-      kn = kn * (uint32_t)P.C + (uint32_t)locate1(v[l], P.L, P.inv_delta, P.C);
+      kn = kn * (uint32_t)P.C + (uint32_t)(P.equi ? locate_g<true>(P, G.edge, v[l]) : locate_g<false>(P, G.edge, v[l]));
     }
     co[s] = kn;
   };
@@ -86,34 +87,6 @@ __global__ void trace_kernel(const DevProblem P, const int i, const uint32_t k, 
 #pragma unroll
     for (int l = 0; l < D; ++l) X[l] = Xn[l];
   }
-}
-
-__global__ void detmath_kernel(const int op, const int64_t n, const double* __restrict__ in,
-                               double* __restrict__ o0, double* __restrict__ o1, const double* __restrict__ det) {
-  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= n) return;
-  DetTabs T;
-  T.logt = reinterpret_cast<const double2*>(det);
-  T.sct = reinterpret_cast<const double2*>(det + 256);
-  if (op == 0) {
-    o0[t] = dm_log(in[t], T);
-  } else {
-    double s, c;
-    dm_sincospi2(in[t], T, s, c);
-    o0[t] = s;
-    o1[t] = c;
-  }
-}
-
-__global__ void philox_kernel(const int64_t n, const uint32_t* __restrict__ ctr, const uint32_t k0,
-                              const uint32_t k1, uint32_t* __restrict__ out) {
-  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= n) return;
-  const U4 o = philox4x32_10(U4{ctr[4 * t], ctr[4 * t + 1], ctr[4 * t + 2], ctr[4 * t + 3]}, k0, k1);
-  out[4 * t] = o.x;
-  out[4 * t + 1] = o.y;
-  out[4 * t + 2] = o.z;
-  out[4 * t + 3] = o.w;
 }
 
 }  // namespace srk

@@ -1,0 +1,40 @@
+// inst.cuh — launch wrappers for one (D, Q) (see ops.h). Included only by the
+// inst_*.cu instantiation units.
+#pragma once
+#include "aux_kernels.cuh"
+#include "ops.h"
+
+using namespace srk;
+
+template <int D, int Q, bool EQ>
+static cudaError_t prepare_impl(int C, int64_t M, bool by_smem, size_t* smem, int* ctas) {
+  *smem = SmemLayout<D, Q>::bytes(C, M, by_smem);
+  cudaError_t e = cudaFuncSetAttribute(step_kernel<D, Q, EQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)*smem);
+  if (e != cudaSuccess) return e;
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(ctas, step_kernel<D, Q, EQ>, kThreads, *smem);
+}
+template <int D, int Q, bool EQ>
+static void step_impl(const DevProblem& P, int i, int64_t kb, int64_t nk, int grid, size_t smem, cudaStream_t s) {
+  step_kernel<D, Q, EQ><<<grid, kThreads, smem, s>>>(P, i, kb, nk);
+}
+template <int D, int Q>
+static void eval_impl(const DevProblem& P, int i, int64_t n, const double* x, double* y, double* z, cudaStream_t s) {
+  const int bs = 128;
+  eval_kernel<D, Q><<<(unsigned)((n + bs - 1) / bs), bs, 0, s>>>(P, i, n, x, y, z);
+}
+template <int D, int Q>
+static void trace_impl(const DevProblem& P, int i, uint32_t k, int64_t m0, int64_t n, double* x, int64_t* c,
+                       double* w, cudaStream_t s) {
+  const int bs = 64;
+  trace_kernel<D, Q><<<(unsigned)((n + bs - 1) / bs), bs, 0, s>>>(P, i, k, m0, n, x, c, w);
+}
+
+template <int D, int Q>
+Ops make_ops() {
+  if constexpr (D <= 8)
+    return Ops{D, Q, prepare_impl<D, Q, false>, step_impl<D, Q, false>, prepare_impl<D, Q, true>, step_impl<D, Q, true>,
+               eval_impl<D, Q>, trace_impl<D, Q>};
+  else
+    return Ops{D, Q, prepare_impl<D, Q, false>, step_impl<D, Q, false>, nullptr, nullptr, eval_impl<D, Q>,
+               trace_impl<D, Q>};
+}

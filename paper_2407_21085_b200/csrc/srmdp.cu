@@ -22,6 +22,8 @@
 #include "../../include/srmdp.h"
 #include "../../include/srmdp_debug.h"
 #include "aux_kernels.cuh"
+#include "debug_kernels.cuh"
+#include "ops.h"
 
 using namespace srk;
 
@@ -169,6 +171,34 @@ static void det_tables(double* out /* 512 */) {
   }
 }
 
+// dm_log (path function of docs/detmath.md) on the host, from the tables.
+static double host_dm_log(double x, const double* det) {
+  if (x != x || x < 0.0) return NAN;
+  if (x == 0.0) return -INFINITY;
+  if (std::isinf(x)) return INFINITY;
+  static const double A[10] = {0.0, 0.0,
+      -0x1.0000000000000p-1, 0x1.5555555555555p-2, -0x1.0000000000000p-2, 0x1.999999999999ap-3,
+      -0x1.5555555555555p-3, 0x1.2492492492492p-3, -0x1.0000000000000p-3, 0x1.c71c71c71c71cp-4};
+  int k = 0;
+  if (x < 0x1p-1022) { x = x * 0x1p54; k = -54; }
+  uint64_t b;
+  memcpy(&b, &x, 8);
+  k = k + (int)(b >> 52) - 1023;
+  const uint64_t mb = b & 0x000fffffffffffffull;
+  const int j = (int)(mb >> 45);
+  const uint64_t m1 = mb | 0x3ff0000000000000ull;
+  double m;
+  memcpy(&m, &m1, 8);
+  if (j >= 53) { m = m * 0.5; k = k + 1; }
+  const double r = std::fma(m, det[2 * j], -1.0);
+  const double r2 = r * r;
+  double p = A[9];
+  for (int n = 8; n >= 2; --n) p = std::fma(p, r, A[n]);
+  const double l1 = std::fma(r2, p, r);
+  const double kd = (double)k;
+  return ((kd * 0x1.62e42fee00000p-1) + det[2 * j + 1]) + (l1 + (kd * 0x1.a39ef35793c76p-33));
+}
+
 // F_nu(x) = 1/(1+exp(-mu x))
 static double host_F(double mu, double x) {
   if (x == -INFINITY) return 0.0;
@@ -177,18 +207,26 @@ static double host_F(double mu, double x) {
 }
 
 // tabs = [F(e_c), c=0..C | e_c, c=0..C | r_c, c=0..C-1 | pad | LOGT | SCT] (problem.cuh)
-static std::vector<double> grid_tables(int C, double L, double mu) {
+// equi: equal-probability breakpoints e_c = -(1/mu) dm_log(C/c - 1) (docs/streams.md §5)
+static std::vector<double> grid_tables(int C, double L, double mu, bool equi) {
   std::vector<double> t(tabs_len(C), 0.0);
-  det_tables(t.data() + tabs_det_off(C));
+  double* det = t.data() + tabs_det_off(C);
+  det_tables(det);
   const double delta = (2.0 * L) / (double)C;
   for (int c = 0; c <= C; ++c) {
-    double e = (c == 0) ? -INFINITY : (c == C) ? INFINITY : ((-L) + ((double)c * delta));
+    double e;
+    if (c == 0) e = -INFINITY;
+    else if (c == C) e = INFINITY;
+    else if (equi) e = (-(1.0 / mu)) * host_dm_log(((double)C / (double)c) - 1.0, det);
+    else e = (-L) + ((double)c * delta);
     t[C + 1 + c] = e;
     t[c] = host_F(mu, e);
   }
+  const double* edge = t.data() + C + 1;
   for (int c = 0; c < C; ++c) {
     double r;
     if (C == 1) r = 0.0;
+    else if (equi) r = (c == 0) ? edge[1] : (c == C - 1) ? edge[C - 1] : (edge[c] + edge[c + 1]) * 0.5;
     else if (c == 0) r = (-L) + (1.0 * delta);
     else if (c == C - 1) r = (-L) + ((double)(C - 1) * delta);
     else r = (-L) + (((double)c + 0.5) * delta);
@@ -198,43 +236,9 @@ static std::vector<double> grid_tables(int C, double L, double mu) {
 }
 
 // ------------------------------------------------------------------------
-// per-(d,q) kernel dispatch
+// per-(d,q) kernel dispatch: the launch wrappers are instantiated in the
+// inst_*.cu translation units (compiled in parallel), see ops.h
 // ------------------------------------------------------------------------
-struct Ops {
-  int D, Q;
-  cudaError_t (*prepare)(int C, int64_t M, bool by_smem, size_t* smem, int* ctas);
-  void (*step)(const DevProblem&, int, int64_t, int64_t, int, size_t, cudaStream_t);
-  void (*eval)(const DevProblem&, int, int64_t, const double*, double*, double*, cudaStream_t);
-  void (*trace)(const DevProblem&, int, uint32_t, int64_t, int64_t, double*, int64_t*, double*, cudaStream_t);
-};
-
-template <int D, int Q>
-static cudaError_t prepare_impl(int C, int64_t M, bool by_smem, size_t* smem, int* ctas) {
-  *smem = SmemLayout<D, Q>::bytes(C, M, by_smem);
-  cudaError_t e = cudaFuncSetAttribute(step_kernel<D, Q>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)*smem);
-  if (e != cudaSuccess) return e;
-  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(ctas, step_kernel<D, Q>, kThreads, *smem);
-}
-template <int D, int Q>
-static void step_impl(const DevProblem& P, int i, int64_t kb, int64_t nk, int grid, size_t smem, cudaStream_t s) {
-  step_kernel<D, Q><<<grid, kThreads, smem, s>>>(P, i, kb, nk);
-}
-template <int D, int Q>
-static void eval_impl(const DevProblem& P, int i, int64_t n, const double* x, double* y, double* z, cudaStream_t s) {
-  const int bs = 128;
-  eval_kernel<D, Q><<<(unsigned)((n + bs - 1) / bs), bs, 0, s>>>(P, i, n, x, y, z);
-}
-template <int D, int Q>
-static void trace_impl(const DevProblem& P, int i, uint32_t k, int64_t m0, int64_t n, double* x, int64_t* c,
-                       double* w, cudaStream_t s) {
-  const int bs = 64;
-  trace_kernel<D, Q><<<(unsigned)((n + bs - 1) / bs), bs, 0, s>>>(P, i, k, m0, n, x, c, w);
-}
-template <int D, int Q>
-static constexpr Ops make_ops() {
-  return Ops{D, Q, prepare_impl<D, Q>, step_impl<D, Q>, eval_impl<D, Q>, trace_impl<D, Q>};
-}
-
 // Compiled (d, q) set: d = q = 1..8 and the paper's high-d rows 11..19
 // (PAPER.md table:LP1d11 .. table:LP1d15_19), plus small d != q for AFFINE.
 static const Ops kOps[] = {
@@ -258,6 +262,7 @@ static const Ops* find_ops(int d, int q) {
 struct srmdp {
   srmdp_config cfg{};
   std::vector<double> params;  // [dyn | theta | g]
+  std::vector<double> tabs;    // host copy of the grid tables
   int d = 0, q = 0, N = 0, C = 0, B = 0, B_pad = 0;
   int64_t K = 0, K_pad = 0, chunk = 0, k_begin = 0, k_end = 0, M = 0;
   double C_y = 0, C_z = 0;
@@ -349,6 +354,9 @@ static srmdp_status validate(const srmdp_config* c, std::string& err) {
   for (int l = 0; l < c->d; ++l) K *= c->cells_per_dim;
   if (K >= 4294967296.0) return bad(SRMDP_E_UNSUPPORTED, "K = C^d >= 2^32 (Philox counter layout)");
   if (!find_ops(c->d, c->q)) return bad(SRMDP_E_UNSUPPORTED, "(d, q) not in the compiled set (srmdp_build_info)");
+  if (c->grid != 0 && c->grid != 1) return bad(SRMDP_E_ARG, "grid must be 0 (equal-size) or 1 (equal-probability)");
+  if (c->grid == 1 && !find_ops(c->d, c->q)->step_eq)
+    return bad(SRMDP_E_UNSUPPORTED, "equal-probability strata are compiled for d <= 8");
   return SRMDP_OK;
 }
 
@@ -386,12 +394,13 @@ static srmdp_status enqueue_sweep(srmdp_t* h) {
         int64_t plan[4];
         srmdp_shard_plan(h->K, h->cfg.world, r, plan);
         if (plan[1] > plan[0]) {
-          h->ops->step(h->dp, i, plan[0], plan[1] - plan[0], h->grid, h->smem, h->stream);
+          (h->cfg.grid ? h->ops->step_eq : h->ops->step)(h->dp, i, plan[0], plan[1] - plan[0], h->grid, h->smem,
+                                                         h->stream);
           ++h->launches_per_solve;
         }
       }
     } else if (nk > 0) {
-      h->ops->step(h->dp, i, h->k_begin, nk, h->grid, h->smem, h->stream);
+      (h->cfg.grid ? h->ops->step_eq : h->ops->step)(h->dp, i, h->k_begin, nk, h->grid, h->smem, h->stream);
       ++h->launches_per_solve;
     }
     CK(h, cudaGetLastError(), "step kernel launch");
@@ -463,7 +472,7 @@ extern "C" srmdp_status srmdp_create(const srmdp_config* cfg, srmdp_t** out) {
   h->sms = prop.multiProcessorCount;
 
   const size_t table_bytes = (size_t)h->N * h->K_pad * h->B_pad * sizeof(double);
-  std::vector<double> tabs = grid_tables(h->C, cfg->L, cfg->mu);
+  std::vector<double> tabs = grid_tables(h->C, cfg->L, cfg->mu, cfg->grid != 0);
   if ((e = cudaMalloc(&h->d_table, table_bytes)) != cudaSuccess) { cuda_fail(h, e, "table alloc"); return fail(SRMDP_E_NOMEM); }
   if ((e = cudaMalloc(&h->d_params, h->params.size() * sizeof(double))) != cudaSuccess ||
       (e = cudaMalloc(&h->d_tabs, tabs.size() * sizeof(double))) != cudaSuccess ||
@@ -473,12 +482,13 @@ extern "C" srmdp_status srmdp_create(const srmdp_config* cfg, srmdp_t** out) {
   }
   cudaMemcpy(h->d_params, h->params.data(), h->params.size() * sizeof(double), cudaMemcpyHostToDevice);
   cudaMemcpy(h->d_tabs, tabs.data(), tabs.size() * sizeof(double), cudaMemcpyHostToDevice);
+  h->tabs = tabs;
 
   // launch configuration: persistent CTAs; the pass-1 pairs (B_m, Y1_m) go to a
   // per-CTA global scratch (L2-resident) so shared memory stays small and the
   // L1 keeps room for the prefetched coefficient blocks (3 CTAs/SM)
   const bool by_smem = false;
-  e = h->ops->prepare(h->C, h->M, by_smem, &h->smem, &h->ctas);
+  e = (cfg->grid ? h->ops->prepare_eq : h->ops->prepare)(h->C, h->M, by_smem, &h->smem, &h->ctas);
   if (e != cudaSuccess || h->ctas < 1) {
     if (e == cudaSuccess) h->err = "step kernel does not fit on an SM";
     else cuda_fail(h, e, "kernel attributes");
@@ -500,6 +510,7 @@ extern "C" srmdp_status srmdp_create(const srmdp_config* cfg, srmdp_t** out) {
   P.nbd = (h->d + 1) / 2; P.nbq = (h->q + 1) / 2;
   P.by_in_smem = by_smem ? 1 : 0;
   P.lp0 = cfg->lp0 ? 1 : 0;
+  P.equi = cfg->grid ? 1 : 0;
   P.K = h->K; P.K_pad = h->K_pad; P.M = h->M;
   P.T = cfg->T;
   P.dt = cfg->T / (double)h->N;
@@ -587,6 +598,14 @@ extern "C" srmdp_status srmdp_solve(srmdp_t* h) {
 }
 
 static void centers_host(const srmdp_t* h, int64_t k, double* r) {
+  if (h->cfg.grid) {                 // equal-probability grid: from the host copy of the tables
+    int64_t rem = k;
+    for (int l = h->d - 1; l >= 0; --l) {
+      r[l] = h->tabs[2 * (h->C + 1) + (int)(rem % h->C)];
+      rem /= h->C;
+    }
+    return;
+  }
   const double L = h->cfg.L;
   const int C = h->C;
   const double delta = (2.0 * L) / (double)C;

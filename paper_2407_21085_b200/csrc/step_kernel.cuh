@@ -144,7 +144,7 @@ __device__ __forceinline__ void prefetch_block(const double* blk) {
 // (ILP); per path the block of X_{j+1} is prefetched into L1, then the
 // increments and Euler step of X_{j+2} are computed (FP64-heavy, independent
 // of the gather), then the block is evaluated.
-template <int D, int Q, int PPT>
+template <int D, int Q, int PPT, bool EQ>
 __device__ __forceinline__ void simulate_paths(const DevProblem& P, const Grid& G, const int (&cc)[D], int i,
                                                uint32_t k, uint32_t m0, double* rows, double (&Bout)[PPT],
                                                double (&Y1out)[PPT]) {
@@ -153,7 +153,7 @@ __device__ __forceinline__ void simulate_paths(const DevProblem& P, const Grid& 
 #pragma unroll
   for (int p = 0; p < PPT; ++p) {
     double* row = rows + p * kThreads * KC::ROW;
-    start_point<D>(P, G, cc, i, k, m0 + p * kThreads, Xn[p]);
+    start_point<D, EQ>(P, G, cc, i, k, m0 + p * kThreads, Xn[p]);
     row[0] = 1.0;
 #pragma unroll
     for (int l = 0; l < D; ++l) row[1 + l] = Xn[p][l] - G.cen[cc[l]];
@@ -185,7 +185,7 @@ __device__ __forceinline__ void simulate_paths(const DevProblem& P, const Grid& 
         uint32_t kn = 0;
 #pragma unroll
         for (int l = 0; l < D; ++l) {
-          c[p][l] = locate1(Xn[p][l], P.L, P.inv_delta, P.C);
+          c[p][l] = locate_g<EQ>(P, G.edge, Xn[p][l]);
           kn = kn * (uint32_t)P.C + (uint32_t)c[p][l];
         }
         blk[p] = P.table + ((size_t)(j + 1) * (size_t)P.K_pad + kn) * (size_t)KC::NBP;
@@ -272,7 +272,9 @@ __device__ void chol_solve(const double* L, const double* r, double* b) {
   }
 }
 
-template <int D, int Q>
+// EQ: equal-probability strata (binary-search locate) — a template parameter so
+// the equal-size grid's hot loop carries no grid branch (a runtime branch cost 4%).
+template <int D, int Q, bool EQ>
 __global__ void __launch_bounds__(kThreads, KCfg<D, Q>::CTAS)
 step_kernel(const DevProblem P, const int i, const int64_t k_begin, const int64_t nk) {
   using KC = KCfg<D, Q>;
@@ -344,7 +346,7 @@ step_kernel(const DevProblem P, const int i, const int64_t k_begin, const int64_
         // paths m0+tid (+ m0+tid+256): rows tid (+ tid+256); a second path past M
         // is simulated (valid counters) but neither stored nor reduced
         double Bv[KC::PPT], Y1[KC::PPT];
-        simulate_paths<D, Q, KC::PPT>(P, G, cc, i, k, (uint32_t)(m0 + tid), sRows + tid * KC::ROW, Bv, Y1);
+        simulate_paths<D, Q, KC::PPT, EQ>(P, G, cc, i, k, (uint32_t)(m0 + tid), sRows + tid * KC::ROW, Bv, Y1);
 #pragma unroll
         for (int p = 0; p < KC::PPT; ++p) {
           const int64_t m = m0 + tid + p * kThreads;
@@ -467,7 +469,7 @@ step_kernel(const DevProblem P, const int i, const int64_t k_begin, const int64_
     for (int p = 0; p < KC::N1; ++p) ry[p] = 0.0;
     for (int64_t m = tid; m < M; m += kThreads) {
       double x[D], a[KC::N1];
-      start_point<D>(P, G, cc, i, k, (uint32_t)m, x);
+      start_point<D, EQ>(P, G, cc, i, k, (uint32_t)m, x);
       a[0] = 1.0;
 #pragma unroll
       for (int l = 0; l < D; ++l) a[1 + l] = x[l] - G.cen[cc[l]];

@@ -50,6 +50,7 @@ class srmdp_config(ctypes.Structure):
         ("rank", ctypes.c_int), ("world", ctypes.c_int), ("nccl_unique_id", ctypes.c_void_p),
         ("device", ctypes.c_int), ("stream", ctypes.c_void_p), ("flags", ctypes.c_int),
         ("lp0", ctypes.c_int),
+        ("grid", ctypes.c_int),
     ]
 
 
@@ -160,6 +161,7 @@ def config_from_workload(w: dict, rank: int = 0, world: int = 1, device: int = 0
     cfg.seed = int(w["seed"]) & 0xFFFFFFFFFFFFFFFF
     cfg.rank, cfg.world, cfg.device, cfg.flags = rank, world, device, flags
     cfg.lp0 = 1 if w.get("basis", "lp1") == "lp0" else 0
+    cfg.grid = 1 if w.get("grid", "uniform") == "equiprobable" else 0
     if nccl_id is not None:
         idbuf = ctypes.create_string_buffer(bytes(nccl_id), 128)
         keep.append(idbuf)

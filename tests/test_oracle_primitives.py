@@ -222,3 +222,25 @@ def test_driver_and_terminal(orc):
     assert abs(P.g(x) - om / (1 + om)) < 1e-15
     z = np.array([0.1, 0.2, -0.05])
     assert abs(P.f(0.0, x, 0.4, z) - z.sum() * (0.4 - 5 / 6)) < 1e-15
+
+
+def test_equiprobable_grid(orc):
+    """(A_Strat.) example ii: breakpoints at the logistic quantiles, so
+    every stratum has nu-mass 1/C; samples stay in their cell (KS vs the
+    conditional law) and locate agrees with the breakpoints."""
+    C, mu = 5, 1.3
+    w = dict(workloads.cfg1(M=3000), C=C, mu=mu, grid="equiprobable")
+    P = orc.Problem(w)
+    F = lambda x: 1 / (1 + np.exp(-mu * x))
+    e = [-math.log(C / c - 1) / mu for c in range(1, C)]
+    for c in range(1, C):
+        assert abs(F(e[c - 1]) - c / C) < 1e-14
+    edges = [-math.inf] + e + [math.inf]
+    for cell in range(C):
+        xs = np.array([P.start_point(0, cell, m)[0] for m in range(3000)])
+        assert all(P.locate([x]) == cell for x in xs)
+        assert np.all(xs >= edges[cell] - 1e-12) and np.all(xs <= edges[cell + 1] + 1e-12)
+        Fl, Fh = F(edges[cell]) if cell else 0.0, F(edges[cell + 1]) if cell < C - 1 else 1.0
+        assert stats.kstest(xs, lambda x: (F(x) - Fl) / (Fh - Fl)).statistic < 1.63 / math.sqrt(3000)
+    for x in (-3.0, -0.2, 0.0, 0.7, 10.0):
+        assert P.locate([x]) == sum(1 for b in e if b <= x)

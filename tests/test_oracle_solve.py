@@ -207,3 +207,17 @@ def test_truncation_binds(orc):
         assert np.any(np.abs(y) == 0.3)
     y, _ = P.eval(tab, 3, x)                       # i = N: g, never truncated
     assert np.any(y > 0.3)
+
+
+def test_bookkeeping_equiprobable_grid(orc):
+    """The deterministic closed form holds on the equal-probability grid too."""
+    w = dict(workloads.bookkeeping(d=2, N=5, C=4, M=40), grid="equiprobable", L=123.0)
+    P = orc.Problem(w)
+    tab, fb = P.solve()
+    assert fb == 0
+    bk, N, dt = w["bk"], 5, 0.2
+    x = np.random.default_rng(3).uniform(-4, 4, size=(200, 2))
+    for i in range(N):
+        y, _ = P.eval(tab, i, x)
+        ex = (1 + bk["r"] * dt) ** (N - i) * (bk["a"] + (x + (N - i) * np.array(bk["beta"]) * dt) @ np.array(bk["w"]))
+        assert np.max(np.abs(y - ex) / np.maximum(np.abs(ex), 1.0)) < 1e-12
