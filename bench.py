@@ -49,7 +49,7 @@ F_NORM = 33
 
 def flops_per_path_step(w):
     d, q = w["d"], w["q"]
-    euler = {"bm": d, "gbm": 4 * d, "affine": d * (2 * d + 2 * q + 2)}[w["dyn"]]
+    euler = {"bm": d, "gbm": 4 * d, "gbm_exact": 30 * d, "affine": d * (2 * d + 2 * q + 2)}[w["dyn"]]
     f_f = {"zero": 0, "linear": q + 3, "paper": q + 4}[w["f"]]
     return q * F_NORM + euler + 3 * d + 2 * (q + 1) * (d + 1) + f_f + 2
 

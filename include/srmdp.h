@@ -54,12 +54,14 @@ typedef enum {
  *  dyn    BM     (q = d): X = W, paper §5.1               params: none
  *         GBM    (q = d): b = mu o x, sigma = diag(s o x)           params: mu[d], s[d]
  *         AFFINE        : b = b0 + B1 x, sigma = S0 (constant)      params: b0[d], B1[d*d], S0[d*q]
+ *         GBM_EXACT (q = d): as GBM, exact transition x e^{(mu-s^2/2)dt + s dW}
+ *                           (Alg. "SDE dynamics")        params: mu[d], s[d]
  *  driver ZERO          : f = 0                                     params: none
  *         LINEAR        : f = a y + theta.z + c                     params: a, c, theta[q]
  *         PAPER         : f = (sum_k z_k)(y - (2+q)/(2q))   params: none
  *  terminal AFFINE      : g = a + w.x                               params: a, w[d]
  *         PAPER         : g = omega/(1+omega), omega = e^{T+sum x} params: none */
-typedef enum { SRMDP_DYN_BM = 0, SRMDP_DYN_GBM = 1, SRMDP_DYN_AFFINE = 2 } srmdp_dyn_kind;
+typedef enum { SRMDP_DYN_BM = 0, SRMDP_DYN_GBM = 1, SRMDP_DYN_AFFINE = 2, SRMDP_DYN_GBM_EXACT = 3 } srmdp_dyn_kind;
 typedef enum { SRMDP_F_ZERO = 0, SRMDP_F_LINEAR = 1, SRMDP_F_PAPER = 2 } srmdp_f_kind;
 typedef enum { SRMDP_G_AFFINE = 0, SRMDP_G_PAPER = 1 } srmdp_g_kind;
 

@@ -22,7 +22,7 @@ _SRC = os.path.join(_HERE, "srmdp_oracle.c")
 _HDR = os.path.join(_HERE, "srmdp_oracle.h")
 _LIB = os.path.join(_HERE, "liboracle_srmdp.so")
 
-DYN = {"bm": 0, "gbm": 1, "affine": 2}
+DYN = {"bm": 0, "gbm": 1, "affine": 2, "gbm_exact": 3}
 FKIND = {"zero": 0, "linear": 1, "paper": 2}
 GKIND = {"affine": 0, "paper": 1}
 

@@ -379,6 +379,14 @@ void or_euler(const or_problem* p, double t, const double* x, const double* dW, 
   int d = p->d, q = p->q;
   if (p->dyn_kind == OR_DYN_BM) {
     for (int l = 0; l < d; l++) xn[l] = x[l] + dW[l];
+  } else if (p->dyn_kind == OR_DYN_GBM_EXACT) {
+    /* Alg. "SDE dynamics": exact transition of dX = mu X dt + s X dW. */
+    const double* mu = p->dyn_params;
+    const double* s = p->dyn_params + d;
+    for (int l = 0; l < d; l++) {
+      double a = mu[l] - (0.5 * (s[l] * s[l]));
+      xn[l] = x[l] * or_dm_exp((a * dt) + (s[l] * dW[l]));
+    }
   } else if (p->dyn_kind == OR_DYN_GBM) {
     const double* mu = p->dyn_params;
     const double* s = p->dyn_params + d;

@@ -21,7 +21,7 @@
 extern "C" {
 #endif
 
-enum { OR_DYN_BM = 0, OR_DYN_GBM = 1, OR_DYN_AFFINE = 2 };
+enum { OR_DYN_BM = 0, OR_DYN_GBM = 1, OR_DYN_AFFINE = 2, OR_DYN_GBM_EXACT = 3 };
 enum { OR_F_ZERO = 0, OR_F_LINEAR = 1, OR_F_PAPER = 2 };
 enum { OR_G_AFFINE = 0, OR_G_PAPER = 1 };
 

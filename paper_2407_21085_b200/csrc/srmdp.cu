@@ -316,7 +316,8 @@ extern "C" srmdp_status srmdp_shard_plan(int64_t K, int world, int rank, int64_t
 }
 
 static int expected_params(int which, int kind, int d, int q) {
-  if (which == 0) return kind == SRMDP_DYN_BM ? 0 : kind == SRMDP_DYN_GBM ? 2 * d : d + d * d + d * q;
+  if (which == 0)
+    return kind == SRMDP_DYN_BM ? 0 : (kind == SRMDP_DYN_GBM || kind == SRMDP_DYN_GBM_EXACT) ? 2 * d : d + d * d + d * q;
   if (which == 1) return kind == SRMDP_F_LINEAR ? 2 + q : 0;
   return kind == SRMDP_G_AFFINE ? 1 + d : 0;
 }
@@ -336,10 +337,11 @@ static srmdp_status validate(const srmdp_config* c, std::string& err) {
   if (((c->world > 1 && !loopback) || (c->flags & SRMDP_FLAG_FORCE_NCCL)) && !c->nccl_unique_id)
     return bad(SRMDP_E_ARG, "the NCCL exchange needs nccl_unique_id");
   if (loopback && (c->flags & SRMDP_FLAG_FORCE_NCCL)) return bad(SRMDP_E_ARG, "LOOPBACK and FORCE_NCCL exclude each other");
-  if (c->dyn.kind < 0 || c->dyn.kind > 2 || c->driver.kind < 0 || c->driver.kind > 2 || c->terminal.kind < 0 ||
+  if (c->dyn.kind < 0 || c->dyn.kind > 3 || c->driver.kind < 0 || c->driver.kind > 2 || c->terminal.kind < 0 ||
       c->terminal.kind > 1)
     return bad(SRMDP_E_ARG, "unknown problem family kind");
-  if ((c->dyn.kind == SRMDP_DYN_BM || c->dyn.kind == SRMDP_DYN_GBM) && c->q != c->d)
+  if ((c->dyn.kind == SRMDP_DYN_BM || c->dyn.kind == SRMDP_DYN_GBM || c->dyn.kind == SRMDP_DYN_GBM_EXACT) &&
+      c->q != c->d)
     return bad(SRMDP_E_ARG, "BM and GBM dynamics need q == d");
   const srmdp_fn* fns[3] = {&c->dyn, &c->driver, &c->terminal};
   for (int w = 0; w < 3; ++w) {

@@ -16,7 +16,7 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("SRMDP_LIB") or os.path.join(_HERE, "libsrmdp_b200.so")   # override: A/B builds
 
-DYN = {"bm": 0, "gbm": 1, "affine": 2}
+DYN = {"bm": 0, "gbm": 1, "affine": 2, "gbm_exact": 3}
 FKIND = {"zero": 0, "linear": 1, "paper": 2}
 GKIND = {"affine": 0, "paper": 1}
 FLAG_NO_GRAPH = 1

@@ -221,3 +221,47 @@ def test_bookkeeping_equiprobable_grid(orc):
         y, _ = P.eval(tab, i, x)
         ex = (1 + bk["r"] * dt) ** (N - i) * (bk["a"] + (x + (N - i) * np.array(bk["beta"]) * dt) @ np.array(bk["w"]))
         assert np.max(np.abs(y - ex) / np.maximum(np.abs(ex), 1.0)) < 1e-12
+
+
+def _bsx_truth(w, i, x):
+    """Exact discrete solution with the exact GBM transition (Alg. SDE dynamics):
+    E[X'] = x e^{mu dt}, E[X' dW] = x s dt e^{mu dt} =>
+    y_i = a(1-r dt)^{N-i} + (e^{mu dt}(1-mu dt))^{N-i} w.x,
+    z_{i,l} = (e^{mu dt}(1-mu dt))^{N-i-1} e^{mu dt} s w_l x_l."""
+    bs, N = w["bs"], w["N"]
+    dt = w["T"] / N
+    e = math.exp(bs["mu"] * dt)
+    b = e * (1 - bs["mu"] * dt)
+    y = bs["a"] * (1 - bs["r"] * dt) ** (N - i) + b ** (N - i) * (x @ np.array(bs["w"]))
+    z = b ** (N - i - 1) * e * np.array(bs["w"]) * bs["s"] * x
+    return y, z
+
+
+def test_exact_gbm_transition(orc):
+    """Alg. 'SDE dynamics': X' = x exp((mu - s^2/2) dt + s dW)."""
+    w = workloads.cfg2_exact(N=4)
+    P = orc.Problem(w)
+    x, dW = np.array([1.3, -0.7]), np.array([0.21, -0.05])
+    got = P.euler(0.0, x, dW)
+    mu, s, dt = 0.05, 0.2, 0.25
+    assert np.allclose(got, x * np.exp((mu - s * s / 2) * dt + s * dW), rtol=1e-15)
+
+
+def test_linear_bs_exact_gbm_unbiased(orc):
+    R = 600
+    base = workloads.cfg2_exact(N=4, C=4, M=64)
+    P0 = orc.Problem(base)
+    pts = cell_points(P0, np.random.default_rng(1), per_cell=1, spread=0.3)
+    ys, zs = [], []
+    for s in range(R):
+        P = orc.Problem(dict(base, seed=300 + s))
+        tab, fb = P.solve()
+        ys.append([P.eval(tab, i, pts)[0] for i in range(base["N"])])
+        zs.append([P.eval(tab, i, pts)[1] for i in range(base["N"])])
+    ys, zs = np.array(ys), np.array(zs)
+    for i in range(base["N"]):
+        ty, tz = _bsx_truth(base, i, pts)
+        for est, tru in ((ys[:, i], ty), (zs[:, i], tz)):
+            t = (est.mean(0) - tru) / (est.std(0, ddof=1) / math.sqrt(R))
+            assert np.max(np.abs(t)) < 5.0, (i, np.max(np.abs(t)))
+            assert 0.4 < np.mean(t ** 2) < 2.5, (i, np.mean(t ** 2))

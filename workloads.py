@@ -7,7 +7,7 @@ families follow the paper's §5.1 benchmark and the
 closed-form cases of DESIGN.md §Inputs.
 
 Parameter layouts (docs/streams.md §7 and include/srmdp.h):
-  dyn "bm": none; "gbm": [mu_0..mu_{d-1}, s_0..s_{d-1}];
+  dyn "bm": none; "gbm" and "gbm_exact": [mu_0..mu_{d-1}, s_0..s_{d-1}];
   "affine": [b0 (d), B1 (d*d row-major), S0 (d*q row-major)]
   f "zero": none; "linear": [a, c, theta_0..theta_{q-1}]  (f = a y + theta.z + c);
   "paper": none  ((sum z)(y - (2+q)/(2q)))
@@ -39,6 +39,11 @@ def cfg2(seed: int = 1, M: int = 1024, N: int = 10, C: int = 20) -> dict:
                 g="affine", g_params=[1.0, 1.0, 1.0], C=C, L=6.5, mu=1.0, M=M,
                 C_y_override=math.inf, C_z_override=math.inf, seed=seed,
                 bs=dict(mu=mu, s=s, r=r, a=1.0, w=[1.0, 1.0]))
+
+
+def cfg2_exact(seed: int = 1, M: int = 1024, N: int = 10, C: int = 20) -> dict:
+    """cfg2 with the exact GBM transition (Alg. "SDE dynamics")."""
+    return dict(cfg2(seed, M, N, C), name="cfg2x", dyn="gbm_exact")
 
 
 def benchmark(d: int, N: int, C: int, M: int, seed: int = 1, name: str = "bench", basis: str = "lp1") -> dict:
