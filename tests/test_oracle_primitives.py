@@ -244,3 +244,23 @@ def test_equiprobable_grid(orc):
         assert stats.kstest(xs, lambda x: (F(x) - Fl) / (Fh - Fl)).statistic < 1.63 / math.sqrt(3000)
     for x in (-3.0, -0.2, 0.0, 0.7, 10.0):
         assert P.locate([x]) == sum(1 for b in e if b <= x)
+
+
+def test_paper_schedules_reproduce_printed_rows():
+    """The caption formulas (workloads.paper_schedule) give every printed #C and M,
+    and K = #C^d on every row of tests/golden/paper_mse_all.txt."""
+    import os
+    rows = [l.split() for l in open(os.path.join(os.path.dirname(__file__), "golden", "paper_mse_all.txt"))
+            if l[0] != "#"]
+    checked = 0
+    for r in rows:
+        d, N, C, K, M, table = int(r[1]), int(r[2]), int(r[3]), int(r[4]), int(r[5]), r[10]
+        assert C ** d == K, r
+        try:
+            c2, m2 = workloads.paper_schedule(table, N)
+        except KeyError:
+            continue                                # d >= 11 tables give #C and M explicitly
+        assert (c2, m2) == (C, M), (r, c2, m2)
+        checked += 1
+    assert checked == 19
+    assert abs(workloads.complexity_domain_L(50) - math.log(50)) < 1e-15

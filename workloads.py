@@ -89,3 +89,35 @@ def path_steps(w: dict) -> int:
     """K*M*N(N+1)/2 — the metric's unit."""
     K = w["C"] ** w["d"]
     return K * w["M"] * w["N"] * (w["N"] + 1) // 2
+
+
+# ---------------------------------------------------------------------------
+# Parameter schedules of the paper's experiments (captions of the MSE tables)
+# and the §4.3 calibration (P:808-852). Inputs only.
+# ---------------------------------------------------------------------------
+def paper_schedule(table: str, N: int) -> tuple[int, int]:
+    """(#C, M) of a table row from its caption formula.
+
+    LP0 d=4 (table:LP0d4): #C = floor(4 sqrt N), M = N^2.
+    LP0 d=6 (table:LP0d6_0 / _1): #C = floor(sqrt N) / floor(2 sqrt N), M = N^2.
+    LP1 d=4 (table:LP1d4): #C = floor(3 sqrt(d sqrt N)) - 5, M = (d+1) N^2.
+    LP1 d=6 (table:LP1d6_1): #C = floor(1.5 sqrt(d sqrt N)) - 3, M = (d+1) N^2.
+    """
+    if table == "table:LP0d4":
+        return int(math.floor(4 * math.sqrt(N))), N * N
+    if table == "table:LP0d6_0":
+        return int(math.floor(math.sqrt(N))), N * N
+    if table == "table:LP0d6_1":
+        return int(math.floor(2 * math.sqrt(N))), N * N
+    if table == "table:LP1d4":
+        d = 4
+        return int(math.floor(3 * math.sqrt(d * math.sqrt(N)))) - 5, (d + 1) * N * N
+    if table == "table:LP1d6_1":
+        d = 6
+        return int(math.floor(1.5 * math.sqrt(d * math.sqrt(N)))) - 3, (d + 1) * N * N
+    raise KeyError(table)
+
+
+def complexity_domain_L(N: int, mu: float = 1.0) -> float:
+    """L = log(N)/mu of the theoretical calibration: nu(R^d \\ [-L,L]^d) <= 2d e^{-mu L} = O(1/N)."""
+    return math.log(N) / mu
