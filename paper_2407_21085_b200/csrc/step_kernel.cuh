@@ -62,17 +62,27 @@ struct KCfg {
 // Shared-memory carve-up (in doubles), shared by host sizing and the kernel.
 template <int D, int Q>
 struct SmemLayout {
+  // The solve-phase arrays (Gram/L, R_Z, beta, R_Y, warp partials, flag) alias
+  // the row tile behind the reduction scratch `red`: they are only live after
+  // the last round of pass 1 and die before the next cell's pass 1. Keeps a
+  // d = 6 CTA at 31 KB, so 3 CTAs/SM fit the 100 KB shared-memory carveout and
+  // L1 keeps ~130 KB for the coefficient hot lines.
   using KC = KCfg<D, Q>;
+  static constexpr int RED = (((KC::USE_MMA ? KC::ITEMS * 64 : KC::PAIRS) > kThreads
+                                   ? (KC::USE_MMA ? KC::ITEMS * 64 : KC::PAIRS)
+                                   : kThreads) + 1) & ~1;
+  static constexpr int SOLVE = KC::N1 * KC::N1 + 2 * KC::NZ + 2 * KC::N1 + (kThreads / 32) * KC::N1 + 2;
+  static_assert(RED + SOLVE <= KC::ROWS * KC::ROW, "solve arrays must fit in the row tile");
   __host__ __device__ static int tabs(int C) { return tabs_len(C); }
   __host__ __device__ static int rows(int C) { return tabs(C); }
-  __host__ __device__ static int L(int C) { return rows(C) + KC::ROWS * KC::ROW; }
+  __host__ __device__ static int L(int C) { return rows(C) + RED; }
   __host__ __device__ static int RZ(int C) { return L(C) + KC::N1 * KC::N1; }
   __host__ __device__ static int BZ(int C) { return RZ(C) + KC::NZ; }
   __host__ __device__ static int BY(int C) { return BZ(C) + KC::NZ; }
   __host__ __device__ static int RY(int C) { return BY(C) + KC::N1; }
   __host__ __device__ static int warp(int C) { return RY(C) + KC::N1; }
   __host__ __device__ static int flag(int C) { return warp(C) + (kThreads / 32) * KC::N1; }
-  __host__ __device__ static int pairs(int C) { return flag(C) + 2; }
+  __host__ __device__ static int pairs(int C) { return (rows(C) + KC::ROWS * KC::ROW + 1) & ~1; }
   __host__ __device__ static size_t bytes(int C, int64_t M, bool by_in_smem) {
     return sizeof(double) * ((size_t)pairs(C) + (by_in_smem ? 2 * (size_t)M : 0));
   }
