@@ -266,6 +266,32 @@ __device__ int cholesky_inplace(double* A) {
   return (mn >= 1e-10 * mx) ? 1 : 0;
 }
 
+// The same factorization by one warp (for d > 8): column j's entries
+// t_r = A[r][j] - sum_{k<j} L[r][k] L[j][k] (k ascending, exactly the serial
+// order) are computed by lanes r = j.. in parallel; bit-identical result.
+template <int N1>
+__device__ int cholesky_warp(double* A, int lane) {
+  double mx = 0.0, mn = 1e300;
+  for (int j = 0; j < N1; ++j) {
+    double tj = 0.0;
+    for (int r = j + lane; r < N1; r += 32) {
+      double t = A[r * N1 + j];
+      for (int kk = 0; kk < j; ++kk) t = t - A[r * N1 + kk] * A[j * N1 + kk];
+      if (r == j) tj = t;
+      else A[r * N1 + j] = t;            // column j below the diagonal: not read by column j itself
+    }
+    const double s = __shfl_sync(0xffffffffu, tj, 0);   // lane 0 owns r = j
+    if (!(s > 0.0)) return 0;
+    const double ljj = sqrt(s);
+    mx = fmax(mx, ljj);
+    mn = fmin(mn, ljj);
+    __syncwarp();
+    for (int r = j + lane; r < N1; r += 32) A[r * N1 + j] = (r == j) ? ljj : A[r * N1 + j] / ljj;
+    __syncwarp();
+  }
+  return (mn >= 1e-10 * mx) ? 1 : 0;
+}
+
 // Solve L L^T b = r (L lower in full storage).
 template <int N1>
 __device__ void chol_solve(const double* L, const double* r, double* b) {
@@ -386,10 +412,19 @@ step_kernel(const DevProblem P, const int i, const int64_t k_begin, const int64_
             const double* pa = sRows + 8 * pb + gid;
             const double* pbp = sRows + 8 * qb + gid;
             double c0 = macc[it][0], c1 = macc[it][1];
-            for (int r0 = rlo_; r0 < rhi_ && r0 < nrows; r0 += 4) {
+            const int rend = rhi_ < nrows ? rhi_ : nrows;
+            int r0 = rlo_;
+#pragma unroll 4
+            for (; r0 + 4 <= rend; r0 += 4) {        // full k-steps: no predicates
+              const double av = pa[(r0 + tig) * KC::ROW];
+              const double bv = pbp[(r0 + tig) * KC::ROW];
+              asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                           : "+d"(c0), "+d"(c1) : "d"(av), "d"(bv));
+            }
+            if (r0 < rend) {                          // ragged last k-step: rows >= nrows are 0
               const int rr = r0 + tig;
-              const double av = (rr < nrows) ? pa[rr * KC::ROW] : 0.0;
-              const double bv = (rr < nrows) ? pbp[rr * KC::ROW] : 0.0;
+              const double av = (rr < rend) ? pa[rr * KC::ROW] : 0.0;
+              const double bv = (rr < rend) ? pbp[rr * KC::ROW] : 0.0;
               asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
                            : "+d"(c0), "+d"(c1) : "d"(av), "d"(bv));
             }
@@ -459,7 +494,14 @@ step_kernel(const DevProblem P, const int i, const int64_t k_begin, const int64_
     }
     }
     __syncthreads();
-    if (tid == 0) sFlag[0] = P.lp0 ? 0 : cholesky_inplace<KC::N1>(sL);   // LP0: means below
+    if constexpr (KC::N1 > 9) {
+      if (tid < 32) {
+        const int okw = P.lp0 ? 0 : cholesky_warp<KC::N1>(sL, tid);
+        if (tid == 0) sFlag[0] = okw;
+      }
+    } else {
+      if (tid == 0) sFlag[0] = P.lp0 ? 0 : cholesky_inplace<KC::N1>(sL);   // LP0: means below
+    }
     __syncthreads();
     const int ok = sFlag[0];
     // ---------------- solve Z ---------------------------------
