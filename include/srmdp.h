@@ -127,6 +127,26 @@ srmdp_status srmdp_coeffs(const srmdp_t* h, int i, int basis, double* out, size_
  * NULL). i == N gives y = g(x) and requires z == NULL. */
 srmdp_status srmdp_eval(const srmdp_t* h, int i, size_t n, const double* x, double* y, double* z);
 
+/* Checkpoint / resume. The sweep state after steps N-1 .. i is exactly the
+ * table slices i .. N-1 (the Philox clouds are stateless), so a solve can be
+ * split and resumed bit-identically (also on another `world`):
+ *  srmdp_solve_steps runs steps i_hi down to i_lo (inclusive) with direct
+ *    launches; i_hi must be N-1 or one below the lowest slice already present
+ *    (solved or loaded). Collective.
+ *  srmdp_table_save writes the present slices to a file: magic "SRMD", then
+ *    int32 {version=1, d, q, N, B_pad, hot_len, i_lo}, int64 K, uint64 seed,
+ *    then (N - i_lo) x K x B_pad little-endian doubles, slices i_lo .. N-1 in
+ *    the device block layout of docs/layout.md (rank-local; call on one rank).
+ *  srmdp_table_load reads such a file into a handle created with the same
+ *    (d, q, N, cells, seed, basis, grid); collective (every rank loads). */
+srmdp_status srmdp_solve_steps(srmdp_t* h, int i_hi, int i_lo);
+srmdp_status srmdp_table_save(const srmdp_t* h, const char* path);
+srmdp_status srmdp_table_load(srmdp_t* h, const char* path);
+
+/* Per-step kernel durations of the last solve in ms, out[i] for step i
+ * (needs SRMDP_FLAG_TIME_KERNELS; steps not run in the last call are 0). */
+srmdp_status srmdp_step_ms(const srmdp_t* h, double* out, int n);
+
 /* Replace the Philox key (docs/streams.md §2) for the next srmdp_solve: a new,
  * independent set of clouds on the same problem (independent runs, e.g. the
  * MSE indicators of eq. mse). Collective (same seed on all ranks). */

@@ -284,6 +284,10 @@ struct srmdp {
   ncclComm_t comm = nullptr;
   bool solved = false;
   int launches_per_solve = 0;
+  int valid_from = 0;          // slices valid_from .. N-1 are present (N: none)
+  int graph_launches = 0;
+  int last_hi = 0, last_lo = 0;
+  std::vector<double> step_ms;
   std::vector<cudaEvent_t> ev;
   srmdp_stats_t st{};
   mutable std::string err = "no error";
@@ -383,13 +387,13 @@ static cudaError_t record_event(srmdp_t* h, cudaEvent_t e) {
                                                : cudaEventRecord(e, h->stream);
 }
 
-static srmdp_status enqueue_sweep(srmdp_t* h) {
+static srmdp_status enqueue_sweep(srmdp_t* h, int i_hi, int i_lo) {
   const bool timed = h->cfg.flags & SRMDP_FLAG_TIME_KERNELS;
   CK(h, cudaMemsetAsync(h->d_lp0, 0, sizeof(unsigned long long), h->stream), "memset");
   const int64_t nk = h->k_end - h->k_begin;
   const bool loopback = h->cfg.flags & SRMDP_FLAG_LOOPBACK;
   h->launches_per_solve = 0;
-  for (int i = h->N - 1; i >= 0; --i) {
+  for (int i = i_hi; i >= i_lo; --i) {
     if (timed) CK(h, record_event(h, h->ev[2 * i]), "event");
     if (loopback) {
       for (int r = 0; r < h->cfg.world; ++r) {   // shards in sequence on one table
@@ -552,11 +556,14 @@ extern "C" srmdp_status srmdp_create(const srmdp_config* cfg, srmdp_t** out) {
     ncclResult_t r = api.CommInitRank(&h->comm, cfg->world, id, cfg->rank);
     if (r != ncclSuccess) { h->err = std::string("ncclCommInitRank: ") + api.GetErrorString(r); return fail(SRMDP_E_NCCL); }
   }
+  h->valid_from = h->N;
   h->st.path_steps = (uint64_t)h->K * (uint64_t)h->M * (uint64_t)h->N * (uint64_t)(h->N + 1) / 2;
   h->st.rank_path_steps = (uint64_t)(h->k_end - h->k_begin) * (uint64_t)h->M * (uint64_t)h->N * (uint64_t)(h->N + 1) / 2;
   *out = h;
   return SRMDP_OK;
 }
+
+static srmdp_status finish_solve(srmdp_t* h, std::chrono::steady_clock::time_point t0);
 
 extern "C" srmdp_status srmdp_solve(srmdp_t* h) {
   if (!h) return SRMDP_E_ARG;
@@ -566,7 +573,7 @@ extern "C" srmdp_status srmdp_solve(srmdp_t* h) {
   if (use_graph) {
     if (!h->graph) {
       CK(h, cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal), "begin capture");
-      srmdp_status s = enqueue_sweep(h);
+      srmdp_status s = enqueue_sweep(h, h->N - 1, 0);
       cudaGraph_t g = nullptr;
       cudaError_t e = cudaStreamEndCapture(h->stream, &g);
       if (s != SRMDP_OK) { if (g) cudaGraphDestroy(g); return s; }
@@ -574,12 +581,20 @@ extern "C" srmdp_status srmdp_solve(srmdp_t* h) {
       e = cudaGraphInstantiate(&h->graph, g, 0);
       cudaGraphDestroy(g);
       if (e != cudaSuccess) return cuda_fail(h, e, "graph instantiate");
+      h->graph_launches = h->launches_per_solve;
     }
     CK(h, cudaGraphLaunch(h->graph, h->stream), "graph launch");
+    h->launches_per_solve = h->graph_launches;
   } else {
-    srmdp_status s = enqueue_sweep(h);
+    srmdp_status s = enqueue_sweep(h, h->N - 1, 0);
     if (s != SRMDP_OK) return s;
   }
+  h->last_hi = h->N - 1;
+  h->last_lo = 0;
+  return finish_solve(h, t0);
+}
+
+static srmdp_status finish_solve(srmdp_t* h, std::chrono::steady_clock::time_point t0) {
   CK(h, cudaStreamSynchronize(h->stream), "solve");
   unsigned long long lp0 = 0;
   CK(h, cudaMemcpy(&lp0, h->d_lp0, sizeof(lp0), cudaMemcpyDeviceToHost), "lp0 count");
@@ -587,14 +602,17 @@ extern "C" srmdp_status srmdp_solve(srmdp_t* h) {
   h->st.kernel_launches = h->launches_per_solve;
   if (h->cfg.flags & SRMDP_FLAG_TIME_KERNELS) {
     double tot = 0;
-    for (int i = 0; i < h->N; ++i) {
+    h->step_ms.assign(h->N, 0.0);
+    for (int i = h->last_lo; i <= h->last_hi; ++i) {
       float ms = 0;
       CK(h, cudaEventElapsedTime(&ms, h->ev[2 * i], h->ev[2 * i + 1]), "event time");
+      h->step_ms[i] = ms;
       tot += ms;
     }
     h->st.kernel_ms = tot;
   }
-  h->solved = true;
+  h->valid_from = h->last_lo;
+  h->solved = (h->valid_from == 0);
   h->st.solve_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
   return SRMDP_OK;
 }
@@ -624,7 +642,7 @@ static void centers_host(const srmdp_t* h, int64_t k, double* r) {
 
 extern "C" srmdp_status srmdp_coeffs(const srmdp_t* h, int i, int basis, double* out, size_t out_len) {
   if (!h) return SRMDP_E_ARG;
-  if (!h->solved) { h->err = "coeffs before solve"; return SRMDP_E_STATE; }
+  if (i < h->valid_from && i >= 0) { h->err = "coeffs: slice not computed (solve first)"; return SRMDP_E_STATE; }
   if (i < 0 || i >= h->N || (basis != 0 && basis != 1) || !out || out_len != (size_t)h->K * h->B) {
     h->err = "coeffs: bad i / basis / out_len (must be K*B)";
     return SRMDP_E_ARG;
@@ -673,7 +691,7 @@ extern "C" srmdp_status srmdp_eval(const srmdp_t* h, int i, size_t n, const doub
     h->err = "eval: bad i, NULL buffer, or z requested at i == N";
     return SRMDP_E_ARG;
   }
-  if (i < h->N && !h->solved) { h->err = "eval before solve"; return SRMDP_E_STATE; }
+  if (i < h->N && i < h->valid_from) { h->err = "eval: slice not computed (solve first)"; return SRMDP_E_STATE; }
   if (n == 0) return SRMDP_OK;
   CK(h, cudaSetDevice(h->cfg.device), "cudaSetDevice");
   const size_t nx = n * h->d, nz = z ? n * h->q : 0;
@@ -707,6 +725,89 @@ extern "C" srmdp_status srmdp_reseed(srmdp_t* h, uint64_t seed) {
     h->graph = nullptr;
   }
   h->solved = false;
+  h->valid_from = h->N;
+  return SRMDP_OK;
+}
+
+extern "C" srmdp_status srmdp_solve_steps(srmdp_t* h, int i_hi, int i_lo) {
+  if (!h) return SRMDP_E_ARG;
+  if (i_hi < i_lo || i_lo < 0 || i_hi >= h->N) { h->err = "solve_steps: need N > i_hi >= i_lo >= 0"; return SRMDP_E_ARG; }
+  if (i_hi != h->N - 1 && i_hi != h->valid_from - 1) {
+    h->err = "solve_steps: i_hi must be N-1 or one below the lowest present slice";
+    return SRMDP_E_STATE;
+  }
+  auto t0 = std::chrono::steady_clock::now();
+  CK(h, cudaSetDevice(h->cfg.device), "cudaSetDevice");
+  srmdp_status s = enqueue_sweep(h, i_hi, i_lo);
+  if (s != SRMDP_OK) return s;
+  h->last_hi = i_hi;
+  h->last_lo = i_lo;
+  return finish_solve(h, t0);
+}
+
+struct SrmdHeader {
+  char magic[4];
+  int32_t version, d, q, N, B_pad, hot, i_lo;
+  int64_t K;
+  uint64_t seed;
+};
+
+extern "C" srmdp_status srmdp_table_save(const srmdp_t* h, const char* path) {
+  if (!h || !path) return SRMDP_E_ARG;
+  if (h->valid_from >= h->N) { h->err = "table_save: no slice present"; return SRMDP_E_STATE; }
+  FILE* f = fopen(path, "wb");
+  if (!f) { h->err = std::string("table_save: cannot open ") + path; return SRMDP_E_ARG; }
+  SrmdHeader hd{{'S', 'R', 'M', 'D'}, 1, h->d, h->q, h->N, h->B_pad, hot_len(h->d), h->valid_from, h->K, h->cfg.seed};
+  bool ok = fwrite(&hd, sizeof(hd), 1, f) == 1;
+  std::vector<double> buf((size_t)h->K * h->B_pad);
+  for (int i = h->valid_from; ok && i < h->N; ++i) {
+    cudaError_t e = cudaMemcpy(buf.data(), h->d_table + (size_t)i * h->K_pad * h->B_pad, buf.size() * sizeof(double),
+                               cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) { fclose(f); return cuda_fail(h, e, "table_save copy"); }
+    ok = fwrite(buf.data(), sizeof(double), buf.size(), f) == buf.size();
+  }
+  ok = (fclose(f) == 0) && ok;
+  if (!ok) { h->err = "table_save: write failed"; return SRMDP_E_ARG; }
+  return SRMDP_OK;
+}
+
+extern "C" srmdp_status srmdp_table_load(srmdp_t* h, const char* path) {
+  if (!h || !path) return SRMDP_E_ARG;
+  FILE* f = fopen(path, "rb");
+  if (!f) { h->err = std::string("table_load: cannot open ") + path; return SRMDP_E_ARG; }
+  SrmdHeader hd;
+  if (fread(&hd, sizeof(hd), 1, f) != 1 || memcmp(hd.magic, "SRMD", 4) != 0 || hd.version != 1) {
+    fclose(f);
+    h->err = "table_load: not an SRMD v1 file";
+    return SRMDP_E_ARG;
+  }
+  if (hd.d != h->d || hd.q != h->q || hd.N != h->N || hd.K != h->K || hd.B_pad != h->B_pad ||
+      hd.hot != hot_len(h->d) || hd.seed != h->cfg.seed || hd.i_lo < 0 || hd.i_lo >= h->N) {
+    fclose(f);
+    h->err = "table_load: file does not match this problem (d, q, N, K, layout, seed)";
+    return SRMDP_E_ARG;
+  }
+  CK(h, cudaSetDevice(h->cfg.device), "cudaSetDevice");
+  std::vector<double> buf((size_t)h->K * h->B_pad);
+  for (int i = hd.i_lo; i < h->N; ++i) {
+    if (fread(buf.data(), sizeof(double), buf.size(), f) != buf.size()) {
+      fclose(f);
+      h->err = "table_load: truncated file";
+      return SRMDP_E_ARG;
+    }
+    cudaError_t e = cudaMemcpy(h->d_table + (size_t)i * h->K_pad * h->B_pad, buf.data(), buf.size() * sizeof(double),
+                               cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) { fclose(f); return cuda_fail(h, e, "table_load copy"); }
+  }
+  fclose(f);
+  h->valid_from = hd.i_lo;
+  h->solved = (hd.i_lo == 0);
+  return SRMDP_OK;
+}
+
+extern "C" srmdp_status srmdp_step_ms(const srmdp_t* h, double* out, int n) {
+  if (!h || !out || n != h->N) return SRMDP_E_ARG;
+  for (int i = 0; i < n; ++i) out[i] = (i < (int)h->step_ms.size()) ? h->step_ms[i] : 0.0;
   return SRMDP_OK;
 }
 

@@ -79,6 +79,10 @@ SIGNATURES = {
     "srmdp_eval": (ctypes.c_int, [_H, ctypes.c_int, ctypes.c_size_t, _PD, _PD, _PD]),
     "srmdp_destroy": (None, [_H]),
     "srmdp_reseed": (ctypes.c_int, [_H, ctypes.c_uint64]),
+    "srmdp_solve_steps": (ctypes.c_int, [_H, ctypes.c_int, ctypes.c_int]),
+    "srmdp_table_save": (ctypes.c_int, [_H, ctypes.c_char_p]),
+    "srmdp_table_load": (ctypes.c_int, [_H, ctypes.c_char_p]),
+    "srmdp_step_ms": (ctypes.c_int, [_H, _PD, ctypes.c_int]),
     "srmdp_last_error": (ctypes.c_char_p, [_H]),
     "srmdp_nccl_unique_id": (ctypes.c_int, [ctypes.c_void_p]),
     "srmdp_stats": (ctypes.c_int, [_H, ctypes.POINTER(srmdp_stats_t)]),
@@ -211,6 +215,24 @@ def srmdp_reseed(h, seed: int):
     _check(library().srmdp_reseed(h, int(seed) & 0xFFFFFFFFFFFFFFFF), h)
 
 
+def srmdp_solve_steps(h, i_hi: int, i_lo: int):
+    _check(library().srmdp_solve_steps(h, i_hi, i_lo), h)
+
+
+def srmdp_table_save(h, path: str):
+    _check(library().srmdp_table_save(h, os.fsencode(path)), h)
+
+
+def srmdp_table_load(h, path: str):
+    _check(library().srmdp_table_load(h, os.fsencode(path)), h)
+
+
+def srmdp_step_ms(h, N: int) -> np.ndarray:
+    out = np.zeros(N)
+    _check(library().srmdp_step_ms(h, _dp(out), N), h)
+    return out
+
+
 def srmdp_destroy(h):
     if h:
         library().srmdp_destroy(h)
@@ -232,6 +254,20 @@ class Solver:
     def reseed(self, seed):
         srmdp_reseed(self.h, seed)
         return self
+
+    def solve_steps(self, i_hi, i_lo):
+        srmdp_solve_steps(self.h, i_hi, i_lo)
+        return self
+
+    def save(self, path):
+        srmdp_table_save(self.h, path)
+
+    def load(self, path):
+        srmdp_table_load(self.h, path)
+        return self
+
+    def step_ms(self):
+        return srmdp_step_ms(self.h, self.N)
 
     def stats(self):
         return srmdp_stats(self.h)
