@@ -45,11 +45,15 @@ def nvcc() -> str:
     return "nvcc"
 
 
-def build(force: bool = False, verbose: bool = False, jobs: int | None = None) -> str:
+def build(force: bool = False, verbose: bool = False, jobs: int | None = None, out: str | None = None,
+          defines: tuple = ()) -> str:
+    """Compile (if stale) into `out` (default: the in-tree LIB). `defines` are
+    extra -D flags for A/B experiment builds."""
+    lib = out or LIB
     dl = deps()
-    stale = force or not os.path.exists(LIB) or max(os.path.getmtime(p) for p in dl) > os.path.getmtime(LIB)
+    stale = force or not os.path.exists(lib) or max(os.path.getmtime(p) for p in dl) > os.path.getmtime(lib)
     if not stale:
-        return LIB
+        return lib
     tmpdir = tempfile.mkdtemp(prefix="srmdp_build_")
     srcs = sources()
     objs = [os.path.join(tmpdir, os.path.basename(s) + ".o") for s in srcs]
@@ -57,7 +61,7 @@ def build(force: bool = False, verbose: bool = False, jobs: int | None = None) -
 
     def compile_one(pair):
         src, obj = pair
-        r = subprocess.run([nvcc(), *NVCC_FLAGS, *extra, "-c", "-o", obj, src], cwd=CSRC,
+        r = subprocess.run([nvcc(), *NVCC_FLAGS, *extra, *["-D" + d for d in defines], "-c", "-o", obj, src], cwd=CSRC,
                            capture_output=True, text=True)
         return src, r
 
@@ -69,14 +73,19 @@ def build(force: bool = False, verbose: bool = False, jobs: int | None = None) -
             sys.stderr.write(r.stdout + r.stderr)
         if r.returncode:
             raise RuntimeError("nvcc failed on %s" % src)
-    tmp = LIB + ".tmp%d" % os.getpid()
+    tmp = lib + ".tmp%d" % os.getpid()
     subprocess.check_call([nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", tmp, *objs, "-ldl"])
-    os.replace(tmp, LIB)
+    os.replace(tmp, lib)
     for o in objs:
         os.remove(o)
     os.rmdir(tmpdir)
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    # python build.py [--force] [-v] [--out PATH] [-DNAME=VALUE ...]
+    args = sys.argv[1:]
+    out = args[args.index("--out") + 1] if "--out" in args else None
+    defs = tuple(a[2:] for a in args if a.startswith("-D"))
+    print(build(force="--force" in args or bool(defs) or out is not None, verbose="-v" in args, out=out,
+                defines=defs))

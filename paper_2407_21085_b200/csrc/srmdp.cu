@@ -504,7 +504,7 @@ extern "C" srmdp_status srmdp_create(const srmdp_config* cfg, srmdp_t** out) {
   const int64_t full = (int64_t)h->ctas * h->sms;
   h->grid = (int)(nk < full ? (nk > 0 ? nk : 1) : full);
   if (!by_smem) {
-    if ((e = cudaMalloc(&h->d_scratch, (size_t)h->grid * h->M * 2 * sizeof(double))) != cudaSuccess) {
+    if ((e = cudaMalloc(&h->d_scratch, (size_t)h->grid * h->M * scratch_stride(h->d) * sizeof(double))) != cudaSuccess) {
       cuda_fail(h, e, "scratch alloc");
       return fail(SRMDP_E_NOMEM);
     }

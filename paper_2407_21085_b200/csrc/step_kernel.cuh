@@ -84,7 +84,7 @@ struct SmemLayout {
   __host__ __device__ static int flag(int C) { return warp(C) + (kThreads / 32) * KC::N1; }
   __host__ __device__ static int pairs(int C) { return (rows(C) + KC::ROWS * KC::ROW + 1) & ~1; }
   __host__ __device__ static size_t bytes(int C, int64_t M, bool by_in_smem) {
-    return sizeof(double) * ((size_t)pairs(C) + (by_in_smem ? 2 * (size_t)M : 0));
+    return sizeof(double) * ((size_t)pairs(C) + (by_in_smem ? (size_t)scratch_stride(D) * (size_t)M : 0));
   }
 };
 
@@ -328,7 +328,8 @@ step_kernel(const DevProblem P, const int i, const int64_t k_begin, const int64_
   double* sRY = sm + SL::RY(C);
   double* sWarp = sm + SL::warp(C);
   int* sFlag = reinterpret_cast<int*>(sm + SL::flag(C));
-  double* BYs = P.by_in_smem ? (sm + SL::pairs(C)) : (P.by_scratch + (size_t)blockIdx.x * (size_t)P.M * 2);
+  constexpr int SB = scratch_stride(D);
+  double* BYs = P.by_in_smem ? (sm + SL::pairs(C)) : (P.by_scratch + (size_t)blockIdx.x * (size_t)P.M * SB);
 
   for (int t = tid; t < tabs_len(C); t += kThreads) sm[t] = P.tabs[t];
 
@@ -391,8 +392,12 @@ step_kernel(const DevProblem P, const int i, const int64_t k_begin, const int64_
             const double sc = Bv[p] * P.inv_dt;
 #pragma unroll
             for (int l = 0; l < Q; ++l) row[1 + D + l] = row[1 + D + l] * sc;   // S_{Z,i} = S_{Y,i+1} dW_i / dt
-            BYs[2 * m] = Bv[p];
-            BYs[2 * m + 1] = Y1[p];
+            BYs[SB * m] = Bv[p];
+            BYs[SB * m + 1] = Y1[p];
+            if constexpr (store_design(D)) {
+#pragma unroll
+              for (int l = 0; l < D; ++l) BYs[SB * m + 2 + l] = row[1 + l];
+            }
           }
         }
       }
@@ -520,11 +525,17 @@ step_kernel(const DevProblem P, const int i, const int64_t k_begin, const int64_
 #pragma unroll
     for (int p = 0; p < KC::N1; ++p) ry[p] = 0.0;
     for (int64_t m = tid; m < M; m += kThreads) {
-      double x[D], a[KC::N1];
-      start_point<D, EQ>(P, G, cc, i, k, (uint32_t)m, x);
+      double a[KC::N1];
       a[0] = 1.0;
+      if constexpr (store_design(D)) {
 #pragma unroll
-      for (int l = 0; l < D; ++l) a[1 + l] = x[l] - G.cen[cc[l]];
+        for (int l = 0; l < D; ++l) a[1 + l] = BYs[SB * m + 2 + l];
+      } else {
+        double x[D];
+        start_point<D, EQ>(P, G, cc, i, k, (uint32_t)m, x);
+#pragma unroll
+        for (int l = 0; l < D; ++l) a[1 + l] = x[l] - G.cen[cc[l]];
+      }
       double zl = 0.0;
       for (int l = 0; l < Q; ++l) {
         double v = 0.0;
@@ -532,7 +543,7 @@ step_kernel(const DevProblem P, const int i, const int64_t k_begin, const int64_
         for (int p = 0; p < KC::N1; ++p) v = fma(sBZ[l * KC::N1 + p], a[p], v);
         zl = fma(zweight(P, l), trunc_L(v, P.C_z), zl);
       }
-      const double Sm = BYs[2 * m] + f_eval(P, BYs[2 * m + 1], zl) * dt;
+      const double Sm = BYs[SB * m] + f_eval(P, BYs[SB * m + 1], zl) * dt;
 #pragma unroll
       for (int p = 0; p < KC::N1; ++p) ry[p] = fma(a[p], Sm, ry[p]);
     }
