@@ -71,7 +71,7 @@ struct SmemLayout {
   static constexpr int RED = (((KC::USE_MMA ? KC::ITEMS * 64 : KC::PAIRS) > kThreads
                                    ? (KC::USE_MMA ? KC::ITEMS * 64 : KC::PAIRS)
                                    : kThreads) + 1) & ~1;
-  static constexpr int SOLVE = KC::N1 * KC::N1 + 2 * KC::NZ + 2 * KC::N1 + (kThreads / 32) * KC::N1 + 2;
+  static constexpr int SOLVE = KC::N1 * KC::N1 + 2 * KC::NZ + 2 * KC::N1 + (kThreads / 32) * KC::N1 + 2 + KC::N1 + 2;
   static_assert(RED + SOLVE <= KC::ROWS * KC::ROW, "solve arrays must fit in the row tile");
   __host__ __device__ static int tabs(int C) { return tabs_len(C); }
   __host__ __device__ static int rows(int C) { return tabs(C); }
@@ -82,6 +82,7 @@ struct SmemLayout {
   __host__ __device__ static int RY(int C) { return BY(C) + KC::N1; }
   __host__ __device__ static int warp(int C) { return RY(C) + KC::N1; }
   __host__ __device__ static int flag(int C) { return warp(C) + (kThreads / 32) * KC::N1; }
+  __host__ __device__ static int W(int C) { return flag(C) + 2; }   // W (d+1) then S
   __host__ __device__ static int pairs(int C) { return (rows(C) + KC::ROWS * KC::ROW + 1) & ~1; }
   __host__ __device__ static size_t bytes(int C, int64_t M, bool by_in_smem) {
     return sizeof(double) * ((size_t)pairs(C) + (by_in_smem ? (size_t)scratch_stride(D) * (size_t)M : 0));
@@ -328,6 +329,8 @@ step_kernel(const DevProblem P, const int i, const int64_t k_begin, const int64_
   double* sRY = sm + SL::RY(C);
   double* sWarp = sm + SL::warp(C);
   int* sFlag = reinterpret_cast<int*>(sm + SL::flag(C));
+  double* sW = sm + SL::W(C);                 // certificate of the fresh Z: W[d+1], S
+  double* sS = sW + KC::N1;
   constexpr int SB = scratch_stride(D);
   double* BYs = P.by_in_smem ? (sm + SL::pairs(C)) : (P.by_scratch + (size_t)blockIdx.x * (size_t)P.M * SB);
 
@@ -392,11 +395,11 @@ step_kernel(const DevProblem P, const int i, const int64_t k_begin, const int64_
             const double sc = Bv[p] * P.inv_dt;
 #pragma unroll
             for (int l = 0; l < Q; ++l) row[1 + D + l] = row[1 + D + l] * sc;   // S_{Z,i} = S_{Y,i+1} dW_i / dt
-            BYs[SB * m] = Bv[p];
-            BYs[SB * m + 1] = Y1[p];
+            BYs[m] = Bv[p];                          // scratch is field-major (coalesced)
+            BYs[M + m] = Y1[p];
             if constexpr (store_design(D)) {
 #pragma unroll
-              for (int l = 0; l < D; ++l) BYs[SB * m + 2 + l] = row[1 + l];
+              for (int l = 0; l < D; ++l) BYs[(2 + l) * M + m] = row[1 + l];
             }
           }
         }
@@ -520,6 +523,23 @@ step_kernel(const DevProblem P, const int i, const int64_t k_begin, const int64_
     }
     __syncthreads();
 
+    // certificate of the fresh Z blocks: W = sum_l w_l beta^{Z_l}, S = max_l ||beta^{Z_l}||_1
+    // (stored in the hot line; also used for z_i in pass 2)
+    if (tid < KC::N1) {
+      double wsum = 0.0;
+      for (int l = 0; l < Q; ++l) wsum = fma(zweight(P, l), sBZ[l * KC::N1 + tid], wsum);
+      sW[tid] = wsum;
+    } else if (tid == KC::N1) {
+      double smax = 0.0;
+      for (int l = 0; l < Q; ++l) {
+        double t = 0.0;
+        for (int p = 0; p < KC::N1; ++p) t += fabs(sBZ[l * KC::N1 + p]);
+        smax = fmax(smax, t);
+      }
+      sS[0] = smax;
+    }
+    __syncthreads();
+
     // ---------------- pass 2: Y responses with the fresh z_i ---
     double ry[KC::N1];
 #pragma unroll
@@ -529,21 +549,30 @@ step_kernel(const DevProblem P, const int i, const int64_t k_begin, const int64_
       a[0] = 1.0;
       if constexpr (store_design(D)) {
 #pragma unroll
-        for (int l = 0; l < D; ++l) a[1 + l] = BYs[SB * m + 2 + l];
+        for (int l = 0; l < D; ++l) a[1 + l] = BYs[(2 + l) * M + m];
       } else {
         double x[D];
         start_point<D, EQ>(P, G, cc, i, k, (uint32_t)m, x);
 #pragma unroll
         for (int l = 0; l < D; ++l) a[1 + l] = x[l] - G.cen[cc[l]];
       }
+      // z_i(x_i) through the certificate of the fresh blocks (as eval_block)
       double zl = 0.0;
-      for (int l = 0; l < Q; ++l) {
-        double v = 0.0;
+      int hm = 0x3ff00000;
 #pragma unroll
-        for (int p = 0; p < KC::N1; ++p) v = fma(sBZ[l * KC::N1 + p], a[p], v);
-        zl = fma(zweight(P, l), trunc_L(v, P.C_z), zl);
+      for (int p = 1; p <= D; ++p) hm = max(hm, __double2hiint(a[p]) & 0x7fffffff);
+      if (sS[0] * __hiloint2double(hm, 0xffffffff) <= P.C_z_safe) {
+#pragma unroll
+        for (int p = 0; p < KC::N1; ++p) zl = fma(sW[p], a[p], zl);
+      } else {
+        for (int l = 0; l < Q; ++l) {
+          double v = 0.0;
+#pragma unroll
+          for (int p = 0; p < KC::N1; ++p) v = fma(sBZ[l * KC::N1 + p], a[p], v);
+          zl = fma(zweight(P, l), trunc_L(v, P.C_z), zl);
+        }
       }
-      const double Sm = BYs[SB * m] + f_eval(P, BYs[SB * m + 1], zl) * dt;
+      const double Sm = BYs[m] + f_eval(P, BYs[M + m], zl) * dt;
 #pragma unroll
       for (int p = 0; p < KC::N1; ++p) ry[p] = fma(a[p], Sm, ry[p]);
     }
@@ -571,27 +600,12 @@ step_kernel(const DevProblem P, const int i, const int64_t k_begin, const int64_
       }
     }
     __syncthreads();
-    // certificate of the hot part: W = sum_l w_l beta^{Z_l}, S = max_l ||beta^{Z_l}||_1
-    if (tid < KC::N1) {
-      double wsum = 0.0;
-      for (int l = 0; l < Q; ++l) wsum = fma(zweight(P, l), sBZ[l * KC::N1 + tid], wsum);
-      sRY[tid] = wsum;
-    } else if (tid == KC::N1) {
-      double smax = 0.0;
-      for (int l = 0; l < Q; ++l) {
-        double t = 0.0;
-        for (int p = 0; p < KC::N1; ++p) t += fabs(sBZ[l * KC::N1 + p]);
-        smax = fmax(smax, t);
-      }
-      sWarp[0] = smax;
-    }
-    __syncthreads();
     double* dst = P.table + ((size_t)i * (size_t)P.K_pad + k) * (size_t)KC::NBP;
     for (int b = tid; b < KC::NBP; b += kThreads) {
       double v = 0.0;
       if (b < KC::N1) v = sBY[b];
-      else if (b < 2 * KC::N1) v = sRY[b - KC::N1];
-      else if (b == 2 * KC::N1) v = sWarp[0];
+      else if (b < 2 * KC::N1) v = sW[b - KC::N1];
+      else if (b == 2 * KC::N1) v = sS[0];
       else if (b >= KC::NH && b < KC::NH + KC::NZ) v = sBZ[b - KC::NH];
       dst[b] = v;
     }
