@@ -115,6 +115,13 @@ srmdp_status srmdp_create(const srmdp_config* cfg, srmdp_t** out);
  * ncclAllGather of slice i (world > 1). Collective; blocks until done. */
 srmdp_status srmdp_solve(srmdp_t* h);
 
+/* srmdp_solve split in two: srmdp_solve_async enqueues the whole sweep on the
+ * handle's stream (one CUDA-graph launch) and returns; srmdp_wait
+ * synchronizes that stream and finalizes srmdp_stats. Lets a caller bracket
+ * the device work with its own CUDA events without host gaps. */
+srmdp_status srmdp_solve_async(srmdp_t* h);
+srmdp_status srmdp_wait(srmdp_t* h);
+
 /* Copy the coefficients of time i (0 <= i < N) to host `out`, K x B doubles,
  * B = (q+1)(d+1), per cell [Y | Z_1 .. Z_q] each (d+1) long (docs/layout.md).
  * basis 1: centered beta (native); basis 0: the paper's raw alpha.

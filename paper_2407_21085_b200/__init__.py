@@ -7,7 +7,7 @@ extension is missing (there is no CPU fallback).
 """
 from .srmdp import (  # noqa: F401
     SrmdpError, Solver, config_from_workload, library, srmdp_build_info, srmdp_coeffs, srmdp_create,
-    srmdp_destroy, srmdp_eval, srmdp_last_error, srmdp_nccl_unique_id, srmdp_reseed, srmdp_shard_plan, srmdp_solve, srmdp_solve_steps, srmdp_step_ms,
+    srmdp_destroy, srmdp_eval, srmdp_last_error, srmdp_nccl_unique_id, srmdp_reseed, srmdp_shard_plan, srmdp_solve, srmdp_solve_async, srmdp_solve_steps, srmdp_wait, srmdp_step_ms,
     srmdp_table_load, srmdp_table_save,
     srmdp_stats,
 )

@@ -286,6 +286,8 @@ struct srmdp {
   int launches_per_solve = 0;
   int valid_from = 0;          // slices valid_from .. N-1 are present (N: none)
   int graph_launches = 0;
+  bool pending = false;
+  std::chrono::steady_clock::time_point t_submit;
   int last_hi = 0, last_lo = 0;
   std::vector<double> step_ms;
   std::vector<cudaEvent_t> ev;
@@ -565,9 +567,9 @@ extern "C" srmdp_status srmdp_create(const srmdp_config* cfg, srmdp_t** out) {
 
 static srmdp_status finish_solve(srmdp_t* h, std::chrono::steady_clock::time_point t0);
 
-extern "C" srmdp_status srmdp_solve(srmdp_t* h) {
+extern "C" srmdp_status srmdp_solve_async(srmdp_t* h) {
   if (!h) return SRMDP_E_ARG;
-  auto t0 = std::chrono::steady_clock::now();
+  h->t_submit = std::chrono::steady_clock::now();
   CK(h, cudaSetDevice(h->cfg.device), "cudaSetDevice");
   const bool use_graph = !(h->cfg.flags & SRMDP_FLAG_NO_GRAPH);
   if (use_graph) {
@@ -591,7 +593,21 @@ extern "C" srmdp_status srmdp_solve(srmdp_t* h) {
   }
   h->last_hi = h->N - 1;
   h->last_lo = 0;
-  return finish_solve(h, t0);
+  h->pending = true;
+  return SRMDP_OK;
+}
+
+extern "C" srmdp_status srmdp_wait(srmdp_t* h) {
+  if (!h) return SRMDP_E_ARG;
+  if (!h->pending) return SRMDP_OK;
+  h->pending = false;
+  return finish_solve(h, h->t_submit);
+}
+
+extern "C" srmdp_status srmdp_solve(srmdp_t* h) {
+  srmdp_status s = srmdp_solve_async(h);
+  if (s != SRMDP_OK) return s;
+  return srmdp_wait(h);
 }
 
 static srmdp_status finish_solve(srmdp_t* h, std::chrono::steady_clock::time_point t0) {

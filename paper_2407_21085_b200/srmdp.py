@@ -75,6 +75,8 @@ _H = ctypes.c_void_p
 SIGNATURES = {
     "srmdp_create": (ctypes.c_int, [ctypes.POINTER(srmdp_config), ctypes.POINTER(_H)]),
     "srmdp_solve": (ctypes.c_int, [_H]),
+    "srmdp_solve_async": (ctypes.c_int, [_H]),
+    "srmdp_wait": (ctypes.c_int, [_H]),
     "srmdp_coeffs": (ctypes.c_int, [_H, ctypes.c_int, ctypes.c_int, _PD, ctypes.c_size_t]),
     "srmdp_eval": (ctypes.c_int, [_H, ctypes.c_int, ctypes.c_size_t, _PD, _PD, _PD]),
     "srmdp_destroy": (None, [_H]),
@@ -186,6 +188,14 @@ def srmdp_solve(h):
     _check(library().srmdp_solve(h), h)
 
 
+def srmdp_solve_async(h):
+    _check(library().srmdp_solve_async(h), h)
+
+
+def srmdp_wait(h):
+    _check(library().srmdp_wait(h), h)
+
+
 def srmdp_stats(h) -> dict:
     s = srmdp_stats_t()
     _check(library().srmdp_stats(h, ctypes.byref(s)), h)
@@ -249,6 +259,14 @@ class Solver:
 
     def solve(self):
         srmdp_solve(self.h)
+        return self
+
+    def solve_async(self):
+        srmdp_solve_async(self.h)
+        return self
+
+    def wait(self):
+        srmdp_wait(self.h)
         return self
 
     def reseed(self, seed):
