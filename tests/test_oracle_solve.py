@@ -265,3 +265,43 @@ def test_linear_bs_exact_gbm_unbiased(orc):
             t = (est.mean(0) - tru) / (est.std(0, ddof=1) / math.sqrt(R))
             assert np.max(np.abs(t)) < 5.0, (i, np.max(np.abs(t)))
             assert 0.4 < np.mean(t ** 2) < 2.5, (i, np.mean(t ** 2))
+
+
+def nested_mc(x0, d, N=2, Mo=3000, Mi=3000, seed=0):
+    """Brute-force nested Monte Carlo of eq. MDP:intro for the §5.1
+    benchmark with N = 2 (SURVEY §8(c) 'Tiny grids'): inner conditional
+    expectations give z_1, y_1 at each outer sample, the outer ones z_0, y_0."""
+    rng = np.random.default_rng(seed)
+    dt = 1.0 / N
+    s = math.sqrt(dt)
+    c = (2 + d) / (2 * d)
+
+    def g(x):
+        return 1 / (1 + np.exp(-(1.0 + x.sum(-1))))
+
+    dW0 = rng.normal(size=(Mo, d)) * s
+    X1 = x0 + dW0
+    dW1 = rng.normal(size=(Mo, Mi, d)) * s
+    gN = g(X1[:, None, :] + dW1)
+    z1 = (gN[..., None] * dW1).mean(1) / dt                      # z_1(X_1)
+    y1 = (gN + z1.sum(-1)[:, None] * (gN - c) * dt).mean(1)       # f_1(X_1, y_2 = g, z_1)
+    z0 = (y1[:, None] * dW0).mean(0) / dt
+    y0 = (y1 + z0.sum() * (y1 - c) * dt).mean()
+    se_y = y1.std() / math.sqrt(Mo)
+    se_z = (y1[:, None] * dW0 / dt).std(0).mean() / math.sqrt(Mo)
+    return y0, z0, se_y, se_z
+
+
+def test_benchmark_d2_vs_nested_monte_carlo(orc):
+    x0 = np.array([0.1, -0.2])
+    y_n, z_n, se_yn, se_zn = nested_mc(x0, 2)
+    ests = []
+    for sd in range(6):
+        P = orc.Problem(workloads.benchmark(d=2, N=2, C=20, M=4096, seed=50 + sd))
+        tab, _ = P.solve()
+        y, z = P.eval(tab, 0, x0[None, :])
+        ests.append((y[0], z[0].mean()))
+    e = np.array(ests)
+    m, se = e.mean(0), e.std(0, ddof=1) / math.sqrt(len(e))
+    assert abs(m[0] - y_n) < 4 * math.hypot(se[0], se_yn) + 3e-3, (m[0], y_n)
+    assert abs(m[1] - z_n.mean()) < 4 * math.hypot(se[1], se_zn) + 1e-2, (m[1], z_n)
