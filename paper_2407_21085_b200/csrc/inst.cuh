@@ -7,8 +7,8 @@
 using namespace srk;
 
 template <int D, int Q, bool EQ>
-static cudaError_t prepare_impl(int C, int64_t M, bool by_smem, size_t* smem, int* ctas) {
-  *smem = SmemLayout<D, Q>::bytes(C, M, by_smem);
+static cudaError_t prepare_impl(int C, size_t* smem, int* ctas) {
+  *smem = SmemLayout<D, Q>::bytes(C);
   cudaError_t e = cudaFuncSetAttribute(step_kernel<D, Q, EQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)*smem);
   if (e != cudaSuccess) return e;
   return cudaOccupancyMaxActiveBlocksPerMultiprocessor(ctas, step_kernel<D, Q, EQ>, kThreads, *smem);

@@ -8,9 +8,9 @@
 
 struct Ops {
   int D, Q;
-  cudaError_t (*prepare)(int C, int64_t M, bool by_smem, size_t* smem, int* ctas);   // equal-size grid
+  cudaError_t (*prepare)(int C, size_t* smem, int* ctas);     // equal-size grid
   void (*step)(const srk::DevProblem&, int, int64_t, int64_t, int, size_t, cudaStream_t);
-  cudaError_t (*prepare_eq)(int C, int64_t M, bool by_smem, size_t* smem, int* ctas);  // equal-probability
+  cudaError_t (*prepare_eq)(int C, size_t* smem, int* ctas);  // equal-probability
   void (*step_eq)(const srk::DevProblem&, int, int64_t, int64_t, int, size_t, cudaStream_t);   // (nullptr: d > 8)
   void (*eval)(const srk::DevProblem&, int, int64_t, const double*, double*, double*, cudaStream_t);
   void (*trace)(const srk::DevProblem&, int, uint32_t, int64_t, int64_t, double*, int64_t*, double*, cudaStream_t);

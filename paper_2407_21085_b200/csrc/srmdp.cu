@@ -32,12 +32,6 @@ using namespace srk;
 // ------------------------------------------------------------------------
 static thread_local std::string g_create_err = "no error";
 
-#define SRMDP_FMT_ERR(dst, ...)                  \
-  do {                                           \
-    char _b[512];                                \
-    snprintf(_b, sizeof(_b), __VA_ARGS__);       \
-    (dst) = _b;                                  \
-  } while (0)
 
 // ------------------------------------------------------------------------
 // NCCL, loaded at run time (libnccl.so.2 is already mapped when torch is)
@@ -492,11 +486,10 @@ extern "C" srmdp_status srmdp_create(const srmdp_config* cfg, srmdp_t** out) {
   cudaMemcpy(h->d_tabs, tabs.data(), tabs.size() * sizeof(double), cudaMemcpyHostToDevice);
   h->tabs = tabs;
 
-  // launch configuration: persistent CTAs; the pass-1 pairs (B_m, Y1_m) go to a
-  // per-CTA global scratch (L2-resident) so shared memory stays small and the
-  // L1 keeps room for the prefetched coefficient blocks (3 CTAs/SM)
-  const bool by_smem = false;
-  e = (cfg->grid ? h->ops->prepare_eq : h->ops->prepare)(h->C, h->M, by_smem, &h->smem, &h->ctas);
+  // launch configuration: persistent CTAs; the pass-2 records go to a per-CTA
+  // global scratch (L2-resident) so shared memory stays small and the L1 keeps
+  // room for the prefetched coefficient blocks (3 CTAs/SM at d <= 8)
+  e = (cfg->grid ? h->ops->prepare_eq : h->ops->prepare)(h->C, &h->smem, &h->ctas);
   if (e != cudaSuccess || h->ctas < 1) {
     if (e == cudaSuccess) h->err = "step kernel does not fit on an SM";
     else cuda_fail(h, e, "kernel attributes");
@@ -505,18 +498,15 @@ extern "C" srmdp_status srmdp_create(const srmdp_config* cfg, srmdp_t** out) {
   const int64_t nk = (cfg->flags & SRMDP_FLAG_LOOPBACK) ? h->chunk : h->k_end - h->k_begin;
   const int64_t full = (int64_t)h->ctas * h->sms;
   h->grid = (int)(nk < full ? (nk > 0 ? nk : 1) : full);
-  if (!by_smem) {
-    if ((e = cudaMalloc(&h->d_scratch, (size_t)h->grid * h->M * scratch_stride(h->d) * sizeof(double))) != cudaSuccess) {
-      cuda_fail(h, e, "scratch alloc");
-      return fail(SRMDP_E_NOMEM);
-    }
+  if ((e = cudaMalloc(&h->d_scratch, (size_t)h->grid * h->M * scratch_stride(h->d) * sizeof(double))) != cudaSuccess) {
+    cuda_fail(h, e, "scratch alloc");
+    return fail(SRMDP_E_NOMEM);
   }
 
   DevProblem& P = h->dp;
   P.d = h->d; P.q = h->q; P.N = h->N; P.C = h->C; P.B = h->B; P.B_pad = h->B_pad;
   P.dyn = cfg->dyn.kind; P.fk = cfg->driver.kind; P.gk = cfg->terminal.kind;
   P.nbd = (h->d + 1) / 2; P.nbq = (h->q + 1) / 2;
-  P.by_in_smem = by_smem ? 1 : 0;
   P.lp0 = cfg->lp0 ? 1 : 0;
   P.equi = cfg->grid ? 1 : 0;
   P.K = h->K; P.K_pad = h->K_pad; P.M = h->M;

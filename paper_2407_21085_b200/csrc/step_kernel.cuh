@@ -34,11 +34,10 @@ struct KCfg {
   static constexpr int NG = N1 * (N1 + 1) / 2;      // Gram entries (upper, incl. diag)
   static constexpr int NZ = Q * N1;                 // Z right-hand-side entries
   static constexpr int E = NG + NZ;
-  static constexpr int PPT = 1;                     // paths per thread per round (2 measured slower on cfg4: 2.43e10 vs 2.65e10)
-  static constexpr int ROWS = kThreads * PPT;       // rows (paths) per round
+  static constexpr int ROWS = kThreads;            // rows (paths) per round: one path per thread
   // resident CTAs per SM (launch bounds): 3 (<= 85 registers) up to d = 8; the
   // high-d kernels keep their d-long state in 128 registers at 2 CTAs/SM
-  static constexpr int CTAS = (PPT == 2 || D > 8) ? 2 : 3;
+  static constexpr int CTAS = (D > 8) ? 2 : 3;
   static constexpr int S = (E <= kThreads) ? (kThreads / E) : 1;  // row slices per entry
   static constexpr int PAIRS = E * S;
   static constexpr int NACC = (PAIRS + kThreads - 1) / kThreads;
@@ -84,9 +83,7 @@ struct SmemLayout {
   __host__ __device__ static int flag(int C) { return warp(C) + (kThreads / 32) * KC::N1; }
   __host__ __device__ static int W(int C) { return flag(C) + 2; }   // W (d+1) then S
   __host__ __device__ static int pairs(int C) { return (rows(C) + KC::ROWS * KC::ROW + 1) & ~1; }
-  __host__ __device__ static size_t bytes(int C, int64_t M, bool by_in_smem) {
-    return sizeof(double) * ((size_t)pairs(C) + (by_in_smem ? (size_t)scratch_stride(D) * (size_t)M : 0));
-  }
+  __host__ __device__ static size_t bytes(int C) { return sizeof(double) * (size_t)pairs(C); }
 };
 
 // Exact evaluation of the q Z blocks: zlin = sum_l w_l T_{C_z}(beta^{Z_l} . a).
@@ -146,102 +143,74 @@ __device__ __forceinline__ void prefetch_block(const double* blk) {
   for (int off = 0; off < NHOT * 8; off += 128) asm volatile("prefetch.global.L1 [%0];" ::"l"((const char*)blk + off));
 }
 
-// PPT paths of cloud (i,k), pass 1: path p of this thread is m0 + p*kThreads
-// and owns shared-memory row `rows + p*kThreads*ROW`. The design row
-// (1, x_i - r_k) and dW_i are written there as soon as they exist, so they do
-// not stay in registers across the Euler chain. Returns per path
-// B = S_{Y,i+1}(x_i) = g(x_N) + sum_{j>i} f_j dt (eq. PsiM) and
-// Y1 = y_{i+1}(x_{i+1}). The PPT paths are independent instruction streams
-// (ILP); per path the block of X_{j+1} is prefetched into L1, then the
-// increments and Euler step of X_{j+2} are computed (FP64-heavy, independent
-// of the gather), then the block is evaluated.
-template <int D, int Q, int PPT, bool EQ>
-__device__ __forceinline__ void simulate_paths(const DevProblem& P, const Grid& G, const int (&cc)[D], int i,
-                                               uint32_t k, uint32_t m0, double* rows, double (&Bout)[PPT],
-                                               double (&Y1out)[PPT]) {
+// One path of cloud (i,k), pass 1 (path m of this thread, shared-memory row
+// `row`). The design row (1, x_i - r_k) and dW_i are written to the row as soon
+// as they exist, so they do not stay in registers across the Euler chain.
+// Returns B = S_{Y,i+1}(x_i) = g(x_N) + sum_{j>i} f_j dt (eq. PsiM) and
+// Y1 = y_{i+1}(x_{i+1}). Software pipeline per step: the block of X_{j+1} is
+// located and prefetched into L1, the increments and Euler step of X_{j+2}
+// are computed (FP64-heavy, independent of the gather), then the block is
+// evaluated. (Two paths per thread for ILP measured slower: 2.43e10 vs 2.65e10.)
+template <int D, int Q, bool EQ>
+__device__ __forceinline__ void simulate_path(const DevProblem& P, const Grid& G, const int (&cc)[D], int i,
+                                              uint32_t k, uint32_t m, double* row, double& Bout, double& Y1out) {
   using KC = KCfg<D, Q>;
-  double Xn[PPT][D];
+  double Xn[D];
+  start_point<D, EQ>(P, G, cc, i, k, m, Xn);
+  row[0] = 1.0;
 #pragma unroll
-  for (int p = 0; p < PPT; ++p) {
-    double* row = rows + p * kThreads * KC::ROW;
-    start_point<D, EQ>(P, G, cc, i, k, m0 + p * kThreads, Xn[p]);
-    row[0] = 1.0;
-#pragma unroll
-    for (int l = 0; l < D; ++l) row[1 + l] = Xn[p][l] - G.cen[cc[l]];
-  }
-#pragma unroll
-  for (int p = 0; p < PPT; ++p) {
-    double* row = rows + p * kThreads * KC::ROW;
+  for (int l = 0; l < D; ++l) row[1 + l] = Xn[l] - G.cen[cc[l]];
+  {
     double dW[Q], X1[D];
-    brownian<Q>(P, G, i, i, k, m0 + p * kThreads, dW);
+    brownian<Q>(P, G, i, i, k, m, dW);
 #pragma unroll
     for (int l = 0; l < Q; ++l) row[1 + D + l] = dW[l];
-    euler<D, Q>(P, Xn[p], dW, X1);
+    euler<D, Q>(P, Xn, dW, X1);
 #pragma unroll
-    for (int l = 0; l < D; ++l) Xn[p][l] = X1[l];
+    for (int l = 0; l < D; ++l) Xn[l] = X1[l];
   }
-  double acc[PPT], zlin[PPT], Y1[PPT], yv[PPT];
-#pragma unroll
-  for (int p = 0; p < PPT; ++p) { acc[p] = 0.0; zlin[p] = 0.0; Y1[p] = 0.0; yv[p] = 0.0; }
+  double acc = 0.0, zlin = 0.0, Y1 = 0.0, yv = 0.0;
   const int N = P.N;
 #pragma unroll 1
   for (int j = i; j < N; ++j) {
     // Xn = X_{j+1}
-    double zn[PPT];
+    double zn = 0.0;
     if (j + 1 < N) {
-      const double* blk[PPT];
-      int c[PPT][D];
+      int c[D];
+      uint32_t kn = 0;
 #pragma unroll
-      for (int p = 0; p < PPT; ++p) {
-        uint32_t kn = 0;
-#pragma unroll
-        for (int l = 0; l < D; ++l) {
-          c[p][l] = locate_g<EQ>(P, G.edge, Xn[p][l]);
-          kn = kn * (uint32_t)P.C + (uint32_t)c[p][l];
-        }
-        blk[p] = P.table + ((size_t)(j + 1) * (size_t)P.K_pad + kn) * (size_t)KC::NBP;
-        prefetch_block<2 * KC::N1 + 1>(blk[p]);
+      for (int l = 0; l < D; ++l) {
+        c[l] = locate_g<EQ>(P, G.edge, Xn[l]);
+        kn = kn * (uint32_t)P.C + (uint32_t)c[l];
       }
-      double Xnn[PPT][D];
-#pragma unroll
-      for (int p = 0; p < PPT; ++p) {
+      const double* blk = P.table + ((size_t)(j + 1) * (size_t)P.K_pad + kn) * (size_t)KC::NBP;
+      prefetch_block<2 * KC::N1 + 1>(blk);
+      double Xnn[D];
+      {
         double dW[Q];
-        brownian<Q>(P, G, i, j + 1, k, m0 + p * kThreads, dW);   // increments of step j+1
-        euler<D, Q>(P, Xn[p], dW, Xnn[p]);
+        brownian<Q>(P, G, i, j + 1, k, m, dW);   // increments of step j+1
+        euler<D, Q>(P, Xn, dW, Xnn);
       }
+      double a[D + 1];
+      a[0] = 1.0;
 #pragma unroll
-      for (int p = 0; p < PPT; ++p) {
-        double a[D + 1];
-        a[0] = 1.0;
+      for (int l = 0; l < D; ++l) a[1 + l] = Xn[l] - G.cen[c[l]];
+      eval_block<D, Q>(P, blk, a, yv, zn);       // y_{j+1}(x_{j+1}), z_{j+1}(x_{j+1})
 #pragma unroll
-        for (int l = 0; l < D; ++l) a[1 + l] = Xn[p][l] - G.cen[c[p][l]];
-        eval_block<D, Q>(P, blk[p], a, yv[p], zn[p]);   // y_{j+1}(x_{j+1}), z_{j+1}(x_{j+1})
-#pragma unroll
-        for (int l = 0; l < D; ++l) Xn[p][l] = Xnn[p][l];
-      }
+      for (int l = 0; l < D; ++l) Xn[l] = Xnn[l];
     } else {
-#pragma unroll
-      for (int p = 0; p < PPT; ++p) {
-        yv[p] = g_eval<D>(P, Xn[p]);               // y_N := g
-        zn[p] = 0.0;
-      }
+      yv = g_eval<D>(P, Xn);                     // y_N := g
     }
-#pragma unroll
-    for (int p = 0; p < PPT; ++p) {
-      if (j == i) {
-        Y1[p] = yv[p];
-      } else {
-        const double fdt = f_eval(P, yv[p], zlin[p]) * P.dt;   // f_j(x_j, y_{j+1}(x_{j+1}), z_j(x_j)) dt
-        acc[p] = acc[p] + fdt;
-      }
-      zlin[p] = zn[p];
+    if (j == i) {
+      Y1 = yv;
+    } else {
+      const double fdt = f_eval(P, yv, zlin) * P.dt;   // f_j(x_j, y_{j+1}(x_{j+1}), z_j(x_j)) dt
+      acc = acc + fdt;
     }
+    zlin = zn;
   }
-#pragma unroll
-  for (int p = 0; p < PPT; ++p) {
-    Bout[p] = yv[p] + acc[p];                      // g(x_N) + sum
-    Y1out[p] = Y1[p];
-  }
+  Bout = yv + acc;                                 // g(x_N) + sum
+  Y1out = Y1;
 }
 
 // Cholesky of the symmetric n x n matrix in A (full storage), lower factor in
@@ -332,7 +301,7 @@ step_kernel(const DevProblem P, const int i, const int64_t k_begin, const int64_
   double* sW = sm + SL::W(C);                 // certificate of the fresh Z: W[d+1], S
   double* sS = sW + KC::N1;
   constexpr int SB = scratch_stride(D);
-  double* BYs = P.by_in_smem ? (sm + SL::pairs(C)) : (P.by_scratch + (size_t)blockIdx.x * (size_t)P.M * SB);
+  double* BYs = P.by_scratch + (size_t)blockIdx.x * (size_t)P.M * SB;   // this CTA's pass-2 records
 
   for (int t = tid; t < tabs_len(C); t += kThreads) sm[t] = P.tabs[t];
 
@@ -382,26 +351,19 @@ step_kernel(const DevProblem P, const int i, const int64_t k_begin, const int64_
     for (int it = 0; it < KC::NI; ++it) macc[it][0] = macc[it][1] = 0.0;
     for (int64_t m0 = 0; m0 < M; m0 += KC::ROWS) {
       const int nrows = (int)((M - m0) < KC::ROWS ? (M - m0) : KC::ROWS);
-      if (m0 + tid < M) {
-        // paths m0+tid (+ m0+tid+256): rows tid (+ tid+256); a second path past M
-        // is simulated (valid counters) but neither stored nor reduced
-        double Bv[KC::PPT], Y1[KC::PPT];
-        simulate_paths<D, Q, KC::PPT, EQ>(P, G, cc, i, k, (uint32_t)(m0 + tid), sRows + tid * KC::ROW, Bv, Y1);
+      const int64_t m = m0 + tid;
+      if (m < M) {
+        double* row = sRows + tid * KC::ROW;
+        double Bv, Y1;
+        simulate_path<D, Q, EQ>(P, G, cc, i, k, (uint32_t)m, row, Bv, Y1);
+        const double sc = Bv * P.inv_dt;
 #pragma unroll
-        for (int p = 0; p < KC::PPT; ++p) {
-          const int64_t m = m0 + tid + p * kThreads;
-          if (m < M) {
-            double* row = sRows + (tid + p * kThreads) * KC::ROW;
-            const double sc = Bv[p] * P.inv_dt;
+        for (int l = 0; l < Q; ++l) row[1 + D + l] = row[1 + D + l] * sc;   // S_{Z,i} = S_{Y,i+1} dW_i / dt
+        BYs[m] = Bv;                               // scratch is field-major (coalesced)
+        BYs[M + m] = Y1;
+        if constexpr (store_design(D)) {
 #pragma unroll
-            for (int l = 0; l < Q; ++l) row[1 + D + l] = row[1 + D + l] * sc;   // S_{Z,i} = S_{Y,i+1} dW_i / dt
-            BYs[m] = Bv[p];                          // scratch is field-major (coalesced)
-            BYs[M + m] = Y1[p];
-            if constexpr (store_design(D)) {
-#pragma unroll
-              for (int l = 0; l < D; ++l) BYs[(2 + l) * M + m] = row[1 + l];
-            }
-          }
+          for (int l = 0; l < D; ++l) BYs[(2 + l) * M + m] = row[1 + l];
         }
       }
       __syncthreads();
