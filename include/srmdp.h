@@ -46,7 +46,8 @@ typedef enum {
   SRMDP_E_CUDA = -4,        /* CUDA runtime error (message has the CUDA string) */
   SRMDP_E_NCCL = -5,        /* NCCL error / library not loadable for world > 1 */
   SRMDP_E_NOMEM = -6,       /* device allocation failed */
-  SRMDP_E_UNSUPPORTED = -7  /* outside the compiled (d,q) set or the counter limits */
+  SRMDP_E_UNSUPPORTED = -7, /* outside the counter / size limits (d, q <= 32, ...) */
+  SRMDP_E_JIT = -8          /* the user-problem / (d,q) NVRTC build failed (message has the log) */
 } srmdp_status;
 
 /* Closed-form problem families (no host callbacks: they cannot run on the
@@ -61,9 +62,37 @@ typedef enum {
  *         PAPER         : f = (sum_k z_k)(y - (2+q)/(2q))   params: none
  *  terminal AFFINE      : g = a + w.x                               params: a, w[d]
  *         PAPER         : g = omega/(1+omega), omega = e^{T+sum x} params: none */
-typedef enum { SRMDP_DYN_BM = 0, SRMDP_DYN_GBM = 1, SRMDP_DYN_AFFINE = 2, SRMDP_DYN_GBM_EXACT = 3 } srmdp_dyn_kind;
-typedef enum { SRMDP_F_ZERO = 0, SRMDP_F_LINEAR = 1, SRMDP_F_PAPER = 2 } srmdp_f_kind;
-typedef enum { SRMDP_G_AFFINE = 0, SRMDP_G_PAPER = 1 } srmdp_g_kind;
+typedef enum { SRMDP_DYN_BM = 0, SRMDP_DYN_GBM = 1, SRMDP_DYN_AFFINE = 2, SRMDP_DYN_GBM_EXACT = 3,
+               SRMDP_DYN_USER = 4 } srmdp_dyn_kind;
+typedef enum { SRMDP_F_ZERO = 0, SRMDP_F_LINEAR = 1, SRMDP_F_PAPER = 2, SRMDP_F_USER = 3 } srmdp_f_kind;
+typedef enum { SRMDP_G_AFFINE = 0, SRMDP_G_PAPER = 1, SRMDP_G_USER = 2 } srmdp_g_kind;
+
+/* User problems (b, sigma, f, g given as code). A *_USER
+ * kind takes n_params = 0 in its srmdp_fn; the functions come from
+ * srmdp_config.user_src, CUDA C++ device code that srmdp_create compiles with
+ * NVRTC for sm_100a together with the step, eval and trace kernels (one
+ * module per distinct (source, d, q, kinds), cached for the process; the
+ * compile takes ~2 s). The source sees SRMDP_D, SRMDP_Q (the problem's d, q)
+ * and SRMDP_USER_FN (the function qualifiers) and defines, for the kinds
+ * selected:
+ *
+ *   SRMDP_USER_FN void   srmdp_user_b    (const double* p, double t, const double* x, double* b);    b[d]
+ *   SRMDP_USER_FN void   srmdp_user_sigma(const double* p, double t, const double* x, double* s);    s[d*q], row-major
+ *   SRMDP_USER_FN double srmdp_user_f    (const double* p, double t, const double* x, double y,
+ *                                         const double* z);                                          z[q]
+ *   SRMDP_USER_FN double srmdp_user_g    (const double* p, const double* x);
+ *
+ * p = user_params (device copy). t = t_j = j*dt. Euler (indices
+ * t_j, X_j, dW_j): x'_l = x_l + ((b_l dt) + sw_l), sw_l = s_l0 dW_0 + ... +
+ * s_l,q-1 dW_{q-1} in that order. f_j(x_j, y_{j+1}(x_{j+1}), z_j(x_j)) as
+ * P:357 with the full truncated z vector; g at t_N. The module is compiled
+ * with --fmad=false: each + - * / written in the source is one IEEE rounding
+ * (as C with -ffp-contract=off), so b and sigma built from those and sqrt
+ * give path states that a C implementation reproduces bit for bit; vendor
+ * transcendentals (exp, log, ...) do not. NVRTC is loaded at run time
+ * (libnvrtc.so.12); without it a user problem fails with SRMDP_E_JIT.
+ * The same NVRTC build serves (d, q) pairs outside the compiled set
+ * (srmdp_build_info) for the closed-form families. */
 
 typedef struct {
   int kind;             /* one of the enums above */
@@ -79,6 +108,7 @@ typedef struct {
 #define SRMDP_FLAG_LOOPBACK     8 /* emulate `world` ranks in this process: each step launches the world
                                      shards one after another on the same table, no NCCL (tests sharding
                                      and padding on one GPU; `rank` is ignored) */
+#define SRMDP_FLAG_JIT         16 /* build the kernels with NVRTC even when (d, q) is compiled in */
 
 typedef struct {
   int d, q, N;          /* state dim, Brownian dim, time steps */
@@ -103,6 +133,9 @@ typedef struct {
   int grid;             /* 0: equal-size cells, breakpoints -L + j*2L/#C (default);
                            1: equal-probability cells under nu, breakpoints F^{-1}(j/#C)
                            ((A_Strat.) example ii; L unused) */
+  const char* user_src;        /* user problem source (see above), or NULL; copied at create */
+  const double* user_params;   /* host array of n_user_params doubles, copied at create */
+  int n_user_params;
 } srmdp_config;
 
 /* Validate, compute C_y/C_z, build the per-dimension breakpoint/F tables,
@@ -188,6 +221,15 @@ srmdp_status srmdp_stats(const srmdp_t* h, srmdp_stats_t* out);
  * `world` ranks (docs/layout.md): out[0] = k_begin, out[1] = k_end,
  * out[2] = chunk, out[3] = K_pad. */
 srmdp_status srmdp_shard_plan(int64_t K, int world, int rank, int64_t out[4]);
+
+/* NVRTC build of the kernels for a user problem (or a (d, q) outside the
+ * compiled set) without a GPU and without loading anything: checks user_src
+ * before srmdp_create. Kinds as in srmdp_config (user_src may be NULL when no
+ * *_USER kind is given). log (may be NULL) receives the NVRTC log or the
+ * error, NUL-terminated and truncated to log_len bytes. SRMDP_OK or
+ * SRMDP_E_JIT (SRMDP_E_ARG for d, q outside 1..32). */
+srmdp_status srmdp_jit_check(int d, int q, int dyn_kind, int f_kind, int g_kind, const char* user_src, char* log,
+                             size_t log_len);
 
 /* Library version / build info string (ABI version, arch, compiled (d,q)). */
 const char* srmdp_build_info(void);

@@ -22,9 +22,9 @@ _SRC = os.path.join(_HERE, "srmdp_oracle.c")
 _HDR = os.path.join(_HERE, "srmdp_oracle.h")
 _LIB = os.path.join(_HERE, "liboracle_srmdp.so")
 
-DYN = {"bm": 0, "gbm": 1, "affine": 2, "gbm_exact": 3}
-FKIND = {"zero": 0, "linear": 1, "paper": 2}
-GKIND = {"affine": 0, "paper": 1}
+DYN = {"bm": 0, "gbm": 1, "affine": 2, "gbm_exact": 3, "user": 4}
+FKIND = {"zero": 0, "linear": 1, "paper": 2, "user": 3}
+GKIND = {"affine": 0, "paper": 1, "user": 2}
 
 CFLAGS = ["-O2", "-ffp-contract=off", "-fno-fast-math", "-fopenmp", "-fPIC", "-shared", "-std=gnu11", "-pthread"]
 
@@ -40,6 +40,33 @@ def build(force: bool = False) -> str:
     return _LIB
 
 
+_PDc = ctypes.POINTER(ctypes.c_double)
+_USER_VEC = ctypes.CFUNCTYPE(None, _PDc, ctypes.c_double, _PDc, _PDc)
+_USER_F = ctypes.CFUNCTYPE(ctypes.c_double, _PDc, ctypes.c_double, _PDc, ctypes.c_double, _PDc)
+_USER_G = ctypes.CFUNCTYPE(ctypes.c_double, _PDc, _PDc)
+
+
+def build_user(src: str, d: int, q: int) -> str:
+    """Compile a user problem's source (include/srmdp.h "User problems") as
+    plain C with the oracle's flags (gcc, -ffp-contract=off: each written
+    operation one rounding). The source is an input of the problem, like a
+    parameter array; it is cached by content hash under the temp directory."""
+    import hashlib
+    import tempfile
+    text = "#include <math.h>\n#define SRMDP_D %d\n#define SRMDP_Q %d\n#define SRMDP_USER_FN\n%s\n" % (d, q, src)
+    h = hashlib.sha1((" ".join(CFLAGS) + text).encode()).hexdigest()[:16]
+    out = os.path.join(tempfile.gettempdir(), "srmdp_oracle_user_%s.so" % h)
+    if not os.path.exists(out):
+        c = out[:-3] + ".%d.c" % os.getpid()
+        with open(c, "w") as f:
+            f.write(text)
+        tmp = out + ".tmp%d" % os.getpid()
+        subprocess.check_call(["gcc", *CFLAGS, "-o", tmp, c, "-lm"])
+        os.replace(tmp, out)
+        os.remove(c)
+    return out
+
+
 class _Problem(ctypes.Structure):
     _fields_ = [
         ("d", ctypes.c_int), ("q", ctypes.c_int), ("N", ctypes.c_int),
@@ -53,6 +80,8 @@ class _Problem(ctypes.Structure):
         ("seed", ctypes.c_uint64),
         ("lp0", ctypes.c_int),
         ("grid", ctypes.c_int),
+        ("user_b", _USER_VEC), ("user_sigma", _USER_VEC), ("user_f", _USER_F), ("user_g", _USER_G),
+        ("user_params", ctypes.POINTER(ctypes.c_double)),
     ]
 
 
@@ -137,6 +166,17 @@ class Problem:
             self.C, float(w["L"]), float(w["mu"]), self.M, cy, cz,
             int(w["seed"]) & 0xFFFFFFFFFFFFFFFF, 1 if w.get("basis", "lp1") == "lp0" else 0,
             1 if w.get("grid", "uniform") == "equiprobable" else 0)
+        if w.get("user_src") is not None:      # user problem: the same source, compiled as C
+            self._user = ctypes.CDLL(build_user(w["user_src"], self.d, self.q))
+            self._up = np.ascontiguousarray(np.asarray(w.get("user_params", [0.0]), dtype=np.float64).ravel())
+            if w["dyn"] == "user":
+                self.s.user_b = _USER_VEC(("srmdp_user_b", self._user))
+                self.s.user_sigma = _USER_VEC(("srmdp_user_sigma", self._user))
+            if w["f"] == "user":
+                self.s.user_f = _USER_F(("srmdp_user_f", self._user))
+            if w["g"] == "user":
+                self.s.user_g = _USER_G(("srmdp_user_g", self._user))
+            self.s.user_params = _dptr(self._up) if self._up.size else None
         self.K = int(lib().or_num_cells(ctypes.byref(self.s)))
         self.B = (self.q + 1) * (self.d + 1)
 

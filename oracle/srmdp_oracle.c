@@ -379,6 +379,17 @@ void or_euler(const or_problem* p, double t, const double* x, const double* dW, 
   int d = p->d, q = p->q;
   if (p->dyn_kind == OR_DYN_BM) {
     for (int l = 0; l < d; l++) xn[l] = x[l] + dW[l];
+  } else if (p->dyn_kind == OR_DYN_USER) {
+    /* user b(t_j, X_j), sigma(t_j, X_j): X + (b dt + sigma dW), sigma dW summed
+     * over p = 0..q-1 in order (srmdp.h "User problems"). */
+    double b[64], sg[64 * 64];
+    p->user_b(p->user_params, t, x, b);
+    p->user_sigma(p->user_params, t, x, sg);
+    for (int l = 0; l < d; l++) {
+      double sw = sg[l * q + 0] * dW[0];
+      for (int pp = 1; pp < q; pp++) sw = sw + (sg[l * q + pp] * dW[pp]);
+      xn[l] = x[l] + ((b[l] * dt) + sw);
+    }
   } else if (p->dyn_kind == OR_DYN_GBM_EXACT) {
     /* Alg. "SDE dynamics": exact transition of dX = mu X dt + s X dW. */
     const double* mu = p->dyn_params;
@@ -413,6 +424,7 @@ void or_euler(const or_problem* p, double t, const double* x, const double* dW, 
  * (P:914), written 1/(1+exp(-(T+sum x))) (reading R22: same value, no overflow). */
 double or_g(const or_problem* p, const double* x) {
   double s = 0.0;
+  if (p->g_kind == OR_G_USER) return p->user_g(p->user_params, x);
   if (p->g_kind == OR_G_AFFINE) {
     s = p->g_params[0];
     for (int l = 0; l < p->d; l++) s = s + p->g_params[1 + l] * x[l];
@@ -426,7 +438,7 @@ double or_g(const or_problem* p, const double* x) {
 /* Driver f_j(x, y, z) = f(t_j, x, y, z) (reading R17).
  * PAPER: (sum_k z_k)(y - (2+q)/(2q)). LINEAR: a y + theta.z + c. */
 double or_f(const or_problem* p, double t, const double* x, double y, const double* z) {
-  (void)t; (void)x;
+  if (p->f_kind == OR_F_USER) return p->user_f(p->user_params, t, x, y, z);
   if (p->f_kind == OR_F_ZERO) return 0.0;
   if (p->f_kind == OR_F_LINEAR) {
     double v = p->f_params[0] * y;

@@ -21,9 +21,15 @@
 extern "C" {
 #endif
 
-enum { OR_DYN_BM = 0, OR_DYN_GBM = 1, OR_DYN_AFFINE = 2, OR_DYN_GBM_EXACT = 3 };
-enum { OR_F_ZERO = 0, OR_F_LINEAR = 1, OR_F_PAPER = 2 };
-enum { OR_G_AFFINE = 0, OR_G_PAPER = 1 };
+enum { OR_DYN_BM = 0, OR_DYN_GBM = 1, OR_DYN_AFFINE = 2, OR_DYN_GBM_EXACT = 3, OR_DYN_USER = 4 };
+enum { OR_F_ZERO = 0, OR_F_LINEAR = 1, OR_F_PAPER = 2, OR_F_USER = 3 };
+enum { OR_G_AFFINE = 0, OR_G_PAPER = 1, OR_G_USER = 2 };
+
+/* User problem functions (OR_*_USER kinds): the caller's C code for b, sigma,
+ * f, g (include/srmdp.h "User problems" states their meaning); p = user_params. */
+typedef void (*or_user_vec_fn)(const double* p, double t, const double* x, double* out);
+typedef double (*or_user_f_fn)(const double* p, double t, const double* x, double y, const double* z);
+typedef double (*or_user_g_fn)(const double* p, const double* x);
 
 typedef struct {
   int d, q, N;            /* P:25-32, P:121 */
@@ -42,6 +48,11 @@ typedef struct {
   uint64_t seed;          /* Philox key, docs/streams.md */
   int lp0;                /* LP0 piecewise-constant basis (eq. lp0:explicit P:700-707) */
   int grid;               /* 0: equal-size cells on [-L,L]; 1: equal-probability cells under nu */
+  or_user_vec_fn user_b;      /* b(t, x) -> b[d]          (OR_DYN_USER) */
+  or_user_vec_fn user_sigma;  /* sigma(t, x) -> s[d*q]    (OR_DYN_USER), row-major */
+  or_user_f_fn user_f;        /* f(t, x, y, z)            (OR_F_USER) */
+  or_user_g_fn user_g;        /* g(x)                     (OR_G_USER) */
+  const double* user_params;
 } or_problem;
 
 /* --- primitives (docs/streams.md, docs/detmath.md) --- */

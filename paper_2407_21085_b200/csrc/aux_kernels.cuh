@@ -80,7 +80,7 @@ __global__ void trace_kernel(const DevProblem P, const int i, const uint32_t k, 
   for (int j = i; j < P.N; ++j) {
     double dW[Q], Xn[D];
     brownian<Q>(P, G, i, j, k, m, dW);
-    euler<D, Q>(P, X, dW, Xn);
+    euler<D, Q>(P, (double)j * P.dt, X, dW, Xn);
 #pragma unroll
     for (int l = 0; l < Q; ++l) wo[(j - i) * Q + l] = dW[l];
     put(j - i + 1, Xn);

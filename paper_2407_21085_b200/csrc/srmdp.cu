@@ -23,6 +23,7 @@
 #include "../../include/srmdp_debug.h"
 #include "aux_kernels.cuh"
 #include "debug_kernels.cuh"
+#include "jit.h"
 #include "ops.h"
 
 using namespace srk;
@@ -271,7 +272,9 @@ struct srmdp {
   double* d_io = nullptr;
   size_t io_cap = 0;
   DevProblem dp{};
-  const Ops* ops = nullptr;
+  const Ops* ops = nullptr;          // static kernels of (d, q), or
+  const JitKernels* jit = nullptr;   // the NVRTC build (user problem / other (d, q))
+  std::string user_src;
   int grid = 0, ctas = 0, sms = 0;
   size_t smem = 0;
   cudaGraphExec_t graph = nullptr;
@@ -317,9 +320,22 @@ extern "C" srmdp_status srmdp_shard_plan(int64_t K, int world, int rank, int64_t
 
 static int expected_params(int which, int kind, int d, int q) {
   if (which == 0)
-    return kind == SRMDP_DYN_BM ? 0 : (kind == SRMDP_DYN_GBM || kind == SRMDP_DYN_GBM_EXACT) ? 2 * d : d + d * d + d * q;
+    return (kind == SRMDP_DYN_BM || kind == SRMDP_DYN_USER) ? 0
+           : (kind == SRMDP_DYN_GBM || kind == SRMDP_DYN_GBM_EXACT) ? 2 * d
+                                                                    : d + d * d + d * q;
   if (which == 1) return kind == SRMDP_F_LINEAR ? 2 + q : 0;
   return kind == SRMDP_G_AFFINE ? 1 + d : 0;
+}
+
+static bool uses_user(const srmdp_config* c) {
+  return c->dyn.kind == SRMDP_DYN_USER || c->driver.kind == SRMDP_F_USER || c->terminal.kind == SRMDP_G_USER;
+}
+
+// NVRTC build needed: a user problem, a (d, q) outside the compiled set, the
+// equal-probability grid above d = 8, or forced (SRMDP_FLAG_JIT).
+static bool needs_jit(const srmdp_config* c) {
+  const Ops* o = find_ops(c->d, c->q);
+  return uses_user(c) || !o || (c->grid == 1 && !o->step_eq) || (c->flags & SRMDP_FLAG_JIT);
 }
 
 static srmdp_status validate(const srmdp_config* c, std::string& err) {
@@ -337,9 +353,12 @@ static srmdp_status validate(const srmdp_config* c, std::string& err) {
   if (((c->world > 1 && !loopback) || (c->flags & SRMDP_FLAG_FORCE_NCCL)) && !c->nccl_unique_id)
     return bad(SRMDP_E_ARG, "the NCCL exchange needs nccl_unique_id");
   if (loopback && (c->flags & SRMDP_FLAG_FORCE_NCCL)) return bad(SRMDP_E_ARG, "LOOPBACK and FORCE_NCCL exclude each other");
-  if (c->dyn.kind < 0 || c->dyn.kind > 3 || c->driver.kind < 0 || c->driver.kind > 2 || c->terminal.kind < 0 ||
-      c->terminal.kind > 1)
+  if (c->dyn.kind < 0 || c->dyn.kind > 4 || c->driver.kind < 0 || c->driver.kind > 3 || c->terminal.kind < 0 ||
+      c->terminal.kind > 2)
     return bad(SRMDP_E_ARG, "unknown problem family kind");
+  if (uses_user(c) && !c->user_src) return bad(SRMDP_E_ARG, "a *_USER kind needs user_src");
+  if (c->n_user_params < 0 || (c->n_user_params > 0 && !c->user_params))
+    return bad(SRMDP_E_ARG, "user_params must hold n_user_params doubles");
   if ((c->dyn.kind == SRMDP_DYN_BM || c->dyn.kind == SRMDP_DYN_GBM || c->dyn.kind == SRMDP_DYN_GBM_EXACT) &&
       c->q != c->d)
     return bad(SRMDP_E_ARG, "BM and GBM dynamics need q == d");
@@ -355,10 +374,8 @@ static srmdp_status validate(const srmdp_config* c, std::string& err) {
   double K = 1;
   for (int l = 0; l < c->d; ++l) K *= c->cells_per_dim;
   if (K >= 4294967296.0) return bad(SRMDP_E_UNSUPPORTED, "K = C^d >= 2^32 (Philox counter layout)");
-  if (!find_ops(c->d, c->q)) return bad(SRMDP_E_UNSUPPORTED, "(d, q) not in the compiled set (srmdp_build_info)");
+  if (c->d > 32 || c->q > 32) return bad(SRMDP_E_UNSUPPORTED, "d, q <= 32");
   if (c->grid != 0 && c->grid != 1) return bad(SRMDP_E_ARG, "grid must be 0 (equal-size) or 1 (equal-probability)");
-  if (c->grid == 1 && !find_ops(c->d, c->q)->step_eq)
-    return bad(SRMDP_E_UNSUPPORTED, "equal-probability strata are compiled for d <= 8");
   return SRMDP_OK;
 }
 
@@ -383,6 +400,27 @@ static cudaError_t record_event(srmdp_t* h, cudaEvent_t e) {
                                                : cudaEventRecord(e, h->stream);
 }
 
+// Step-kernel attributes and residency: the static instantiation or the NVRTC
+// build (sized with the same step_smem_bytes formula).
+static cudaError_t prepare_step(srmdp_t* h) {
+  if (!h->jit) return (h->cfg.grid ? h->ops->prepare_eq : h->ops->prepare)(h->C, &h->smem, &h->ctas);
+  const void* k = (const void*)h->jit->step[h->cfg.grid ? 1 : 0];
+  h->smem = step_smem_bytes(h->d, h->q, h->C);
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->smem);
+  if (e != cudaSuccess) return e;
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(&h->ctas, k, kThreads, h->smem);
+}
+
+static void launch_step(srmdp_t* h, int i, int64_t kb, int64_t nk) {
+  if (!h->jit) {
+    (h->cfg.grid ? h->ops->step_eq : h->ops->step)(h->dp, i, kb, nk, h->grid, h->smem, h->stream);
+    return;
+  }
+  void* args[] = {&h->dp, &i, &kb, &nk};
+  cudaLaunchKernel((const void*)h->jit->step[h->cfg.grid ? 1 : 0], dim3(h->grid), dim3(kThreads), args, h->smem,
+                   h->stream);   // errors surface through cudaGetLastError below
+}
+
 static srmdp_status enqueue_sweep(srmdp_t* h, int i_hi, int i_lo) {
   const bool timed = h->cfg.flags & SRMDP_FLAG_TIME_KERNELS;
   CK(h, cudaMemsetAsync(h->d_lp0, 0, sizeof(unsigned long long), h->stream), "memset");
@@ -396,13 +434,12 @@ static srmdp_status enqueue_sweep(srmdp_t* h, int i_hi, int i_lo) {
         int64_t plan[4];
         srmdp_shard_plan(h->K, h->cfg.world, r, plan);
         if (plan[1] > plan[0]) {
-          (h->cfg.grid ? h->ops->step_eq : h->ops->step)(h->dp, i, plan[0], plan[1] - plan[0], h->grid, h->smem,
-                                                         h->stream);
+          launch_step(h, i, plan[0], plan[1] - plan[0]);
           ++h->launches_per_solve;
         }
       }
     } else if (nk > 0) {
-      (h->cfg.grid ? h->ops->step_eq : h->ops->step)(h->dp, i, h->k_begin, nk, h->grid, h->smem, h->stream);
+      launch_step(h, i, h->k_begin, nk);
       ++h->launches_per_solve;
     }
     CK(h, cudaGetLastError(), "step kernel launch");
@@ -438,6 +475,19 @@ extern "C" srmdp_status srmdp_create(const srmdp_config* cfg, srmdp_t** out) {
   h->k_begin = plan[0]; h->k_end = plan[1]; h->chunk = plan[2]; h->K_pad = plan[3];
   if (cfg->flags & SRMDP_FLAG_LOOPBACK) { h->k_begin = 0; h->k_end = h->K; }
   h->ops = find_ops(h->d, h->q);
+  if (needs_jit(cfg)) {
+    h->user_src = cfg->user_src ? cfg->user_src : "";
+    std::string jerr;
+    h->jit = jit_kernels(h->d, h->q, cfg->dyn.kind == SRMDP_DYN_USER, cfg->driver.kind == SRMDP_F_USER,
+                         cfg->terminal.kind == SRMDP_G_USER, h->user_src, jerr);
+    if (!h->jit) {
+      g_create_err = jerr;
+      delete h;
+      return SRMDP_E_JIT;
+    }
+    h->ops = nullptr;
+  }
+  h->cfg.user_src = nullptr;
   // truncation constants: override, else eq. prop:bound (reading R5)
   double by, bz;
   bool ok;
@@ -445,14 +495,18 @@ extern "C" srmdp_status srmdp_create(const srmdp_config* cfg, srmdp_t** out) {
   h->smallness_ok = ok;
   h->C_y = std::isnan(cfg->C_y_override) ? by : cfg->C_y_override;
   h->C_z = std::isnan(cfg->C_z_override) ? bz : cfg->C_z_override;
-  // deep-copy parameters: [dyn | theta | g]
+  // deep-copy parameters: [dyn | theta | g | user]
   const int nd = cfg->dyn.n_params, nf = cfg->driver.n_params, ng = cfg->terminal.n_params;
-  h->params.assign(nd + (nf > 2 ? nf - 2 : 0) + ng + 1, 0.0);
+  const int nu = cfg->n_user_params;
+  h->params.assign(nd + (nf > 2 ? nf - 2 : 0) + ng + nu + 1, 0.0);
   for (int t = 0; t < nd; ++t) h->params[t] = cfg->dyn.params[t];
   for (int t = 2; t < nf; ++t) h->params[nd + t - 2] = cfg->driver.params[t];
   const int goff = nd + (nf > 2 ? nf - 2 : 0);
   for (int t = 0; t < ng; ++t) h->params[goff + t] = cfg->terminal.params[t];
+  const int uoff = goff + ng;
+  for (int t = 0; t < nu; ++t) h->params[uoff + t] = cfg->user_params[t];
   h->cfg.dyn.params = h->cfg.driver.params = h->cfg.terminal.params = nullptr;
+  h->cfg.user_params = nullptr;
   h->cfg.nccl_unique_id = nullptr;
 
   auto fail = [&](srmdp_status s) {
@@ -489,7 +543,7 @@ extern "C" srmdp_status srmdp_create(const srmdp_config* cfg, srmdp_t** out) {
   // launch configuration: persistent CTAs; the pass-2 records go to a per-CTA
   // global scratch (L2-resident) so shared memory stays small and the L1 keeps
   // room for the prefetched coefficient blocks (3 CTAs/SM at d <= 8)
-  e = (cfg->grid ? h->ops->prepare_eq : h->ops->prepare)(h->C, &h->smem, &h->ctas);
+  e = prepare_step(h);
   if (e != cudaSuccess || h->ctas < 1) {
     if (e == cudaSuccess) h->err = "step kernel does not fit on an SM";
     else cuda_fail(h, e, "kernel attributes");
@@ -531,6 +585,7 @@ extern "C" srmdp_status srmdp_create(const srmdp_config* cfg, srmdp_t** out) {
   P.dyn_params = h->d_params;
   P.theta = h->d_params + nd;
   P.g_params = h->d_params + goff;
+  P.user_params = h->d_params + uoff;
   P.tabs = h->d_tabs;
   P.table = h->d_table;
   P.by_scratch = h->d_scratch;
@@ -707,7 +762,16 @@ extern "C" srmdp_status srmdp_eval(const srmdp_t* h, int i, size_t n, const doub
   double* dy = dx + nx;
   double* dz = z ? dy + n : nullptr;
   CK(h, cudaMemcpyAsync(dx, x, nx * sizeof(double), cudaMemcpyHostToDevice, h->stream), "eval h2d");
-  h->ops->eval(h->dp, i, (int64_t)n, dx, dy, dz, h->stream);
+  if (h->jit) {
+    const int bs = 128;
+    int ii = i;
+    int64_t nn = (int64_t)n;
+    void* args[] = {const_cast<DevProblem*>(&h->dp), &ii, &nn, &dx, &dy, &dz};
+    CK(h, cudaLaunchKernel((const void*)h->jit->eval, dim3((unsigned)((n + bs - 1) / bs)), dim3(bs), args, 0, h->stream),
+       "eval kernel");
+  } else {
+    h->ops->eval(h->dp, i, (int64_t)n, dx, dy, dz, h->stream);
+  }
   CK(h, cudaGetLastError(), "eval kernel");
   CK(h, cudaMemcpyAsync(y, dy, n * sizeof(double), cudaMemcpyDeviceToHost, h->stream), "eval d2h");
   if (z) CK(h, cudaMemcpyAsync(z, dz, nz * sizeof(double), cudaMemcpyDeviceToHost, h->stream), "eval d2h");
@@ -860,11 +924,28 @@ extern "C" srmdp_status srmdp_stats(const srmdp_t* h, srmdp_stats_t* out) {
   return SRMDP_OK;
 }
 
+extern "C" srmdp_status srmdp_jit_check(int d, int q, int dyn_kind, int f_kind, int g_kind, const char* user_src,
+                                        char* log, size_t log_len) {
+  if (d < 1 || q < 1 || d > 32 || q > 32) return SRMDP_E_ARG;
+  std::string err;
+  size_t bytes = 0;
+  const bool ok = jit_compile_check(d, q, dyn_kind == SRMDP_DYN_USER, f_kind == SRMDP_F_USER, g_kind == SRMDP_G_USER,
+                                    user_src ? user_src : "", err, &bytes);
+  if (ok) err = "ok: " + std::to_string(bytes) + " bytes of sm_100a CUBIN";
+  if (log && log_len) {
+    const size_t n = err.size() < log_len - 1 ? err.size() : log_len - 1;
+    memcpy(log, err.data(), n);
+    log[n] = '\0';
+  }
+  return ok ? SRMDP_OK : SRMDP_E_JIT;
+}
+
 extern "C" const char* srmdp_build_info(void) {
   static std::string info;
   if (info.empty()) {
     info = "srmdp ABI " + std::to_string(SRMDP_ABI_VERSION) + "; sm_100a fp64; (d,q) =";
     for (const Ops& o : kOps) info += " (" + std::to_string(o.D) + "," + std::to_string(o.Q) + ")";
+    info += "; NVRTC: user problems and any other d, q <= 32";
   }
   return info.c_str();
 }
@@ -883,7 +964,16 @@ extern "C" srmdp_status srmdp_debug_trace(const srmdp_t* h, int i, int64_t k, in
   double* dx = h->d_io;
   int64_t* dc = reinterpret_cast<int64_t*>(dx + nx);
   double* dw = dx + nx + nc;
-  h->ops->trace(h->dp, i, (uint32_t)k, m0, n, dx, dc, dw, h->stream);
+  if (h->jit) {
+    const int bs = 64;
+    int ii = i;
+    uint32_t kk = (uint32_t)k;
+    void* args[] = {const_cast<DevProblem*>(&h->dp), &ii, &kk, &m0, &n, &dx, &dc, &dw};
+    CK(h, cudaLaunchKernel((const void*)h->jit->trace, dim3((unsigned)((n + bs - 1) / bs)), dim3(bs), args, 0, h->stream),
+       "trace kernel");
+  } else {
+    h->ops->trace(h->dp, i, (uint32_t)k, m0, n, dx, dc, dw, h->stream);
+  }
   CK(h, cudaGetLastError(), "trace kernel");
   CK(h, cudaMemcpyAsync(x, dx, nx * sizeof(double), cudaMemcpyDeviceToHost, h->stream), "trace d2h");
   CK(h, cudaMemcpyAsync(cell, dc, nc * sizeof(int64_t), cudaMemcpyDeviceToHost, h->stream), "trace d2h");

@@ -25,6 +25,15 @@ namespace srk {
 
 constexpr int kThreads = 256;
 
+// Row stride (doubles) of the shared-memory row tile [1 | x - r_k | S dW/dt]:
+// odd (spreads banks). Dynamic shared memory of the step kernel for (d, q, C):
+// the grid tables then the row tile (the solve arrays alias the tile). Plain
+// functions so the host sizes NVRTC-built kernels with the same formula.
+__host__ __device__ constexpr int row_stride(int d, int q) { return (1 + d + q) | 1; }
+__host__ __device__ constexpr size_t step_smem_bytes(int d, int q, int C) {
+  return sizeof(double) * (size_t)((tabs_len(C) + kThreads * row_stride(d, q) + 1) & ~1);
+}
+
 template <int D, int Q>
 struct KCfg {
   static constexpr int N1 = D + 1;
@@ -37,7 +46,10 @@ struct KCfg {
   static constexpr int ROWS = kThreads;            // rows (paths) per round: one path per thread
   // resident CTAs per SM (launch bounds): 3 (<= 85 registers) up to d = 8; the
   // high-d kernels keep their d-long state in 128 registers at 2 CTAs/SM
-  static constexpr int CTAS = (D > 8) ? 2 : 3;
+#ifndef SRMDP_CTAS_LO
+#define SRMDP_CTAS_LO 3
+#endif
+  static constexpr int CTAS = (D > 8) ? 2 : SRMDP_CTAS_LO;
   static constexpr int S = (E <= kThreads) ? (kThreads / E) : 1;  // row slices per entry
   static constexpr int PAIRS = E * S;
   static constexpr int NACC = (PAIRS + kThreads - 1) / kThreads;
@@ -54,7 +66,7 @@ struct KCfg {
   static constexpr int NI = (ITEMS + NW - 1) / NW;  // items per warp
   // odd row stride (spreads banks); MMA fragment loads of the padding columns
   // (>= NCOL) read neighbouring smem and only feed discarded outputs
-  static constexpr int ROW = NCOL | 1;
+  static constexpr int ROW = row_stride(D, Q);
   static constexpr bool UNROLL_GATHER = (NB <= 128);
 };
 
@@ -82,8 +94,7 @@ struct SmemLayout {
   __host__ __device__ static int warp(int C) { return RY(C) + KC::N1; }
   __host__ __device__ static int flag(int C) { return warp(C) + (kThreads / 32) * KC::N1; }
   __host__ __device__ static int W(int C) { return flag(C) + 2; }   // W (d+1) then S
-  __host__ __device__ static int pairs(int C) { return (rows(C) + KC::ROWS * KC::ROW + 1) & ~1; }
-  __host__ __device__ static size_t bytes(int C) { return sizeof(double) * (size_t)pairs(C); }
+  __host__ __device__ static size_t bytes(int C) { return step_smem_bytes(D, Q, C); }
 };
 
 // Exact evaluation of the q Z blocks: zlin = sum_l w_l T_{C_z}(beta^{Z_l} . a).
@@ -165,7 +176,7 @@ __device__ __forceinline__ void simulate_path(const DevProblem& P, const Grid& G
     brownian<Q>(P, G, i, i, k, m, dW);
 #pragma unroll
     for (int l = 0; l < Q; ++l) row[1 + D + l] = dW[l];
-    euler<D, Q>(P, Xn, dW, X1);
+    euler<D, Q>(P, (double)i * P.dt, Xn, dW, X1);
 #pragma unroll
     for (int l = 0; l < D; ++l) Xn[l] = X1[l];
   }
@@ -189,7 +200,7 @@ __device__ __forceinline__ void simulate_path(const DevProblem& P, const Grid& G
       {
         double dW[Q];
         brownian<Q>(P, G, i, j + 1, k, m, dW);   // increments of step j+1
-        euler<D, Q>(P, Xn, dW, Xnn);
+        euler<D, Q>(P, (double)(j + 1) * P.dt, Xn, dW, Xnn);
       }
       double a[D + 1];
       a[0] = 1.0;
@@ -212,6 +223,74 @@ __device__ __forceinline__ void simulate_path(const DevProblem& P, const Grid& G
   Bout = yv + acc;                                 // g(x_N) + sum
   Y1out = Y1;
 }
+
+#if SRMDP_USER_F
+// Pass 1 of one path for a user driver f(t, x, y, z) that reads the whole
+// truncated z vector, t and x (srmdp.h, SRMDP_F_USER): the plain order of
+// Alg. SRMDP -- per step the increments, the Euler step, then
+// y_{j+1}, z_{j+1} at x_{j+1} from the full block, f_j(x_j, y_{j+1}, z_j(x_j)).
+template <int D, int Q, bool EQ>
+__device__ __forceinline__ void simulate_path_user(const DevProblem& P, const Grid& G, const int (&cc)[D], int i,
+                                                   uint32_t k, uint32_t m, double* row, double& Bout, double& Y1out) {
+  using KC = KCfg<D, Q>;
+  double X[D];
+  start_point<D, EQ>(P, G, cc, i, k, m, X);
+  row[0] = 1.0;
+#pragma unroll
+  for (int l = 0; l < D; ++l) row[1 + l] = X[l] - G.cen[cc[l]];
+  double zc[Q];
+#pragma unroll
+  for (int l = 0; l < Q; ++l) zc[l] = 0.0;
+  double acc = 0.0, Y1 = 0.0, yv = 0.0;
+  const int N = P.N;
+#pragma unroll 1
+  for (int j = i; j < N; ++j) {
+    const double tj = (double)j * P.dt;
+    double dW[Q], Xn[D], zn[Q];
+    brownian<Q>(P, G, i, j, k, m, dW);
+    if (j == i) {
+#pragma unroll
+      for (int l = 0; l < Q; ++l) row[1 + D + l] = dW[l];
+    }
+    euler<D, Q>(P, tj, X, dW, Xn);
+    if (j + 1 < N) {
+      uint32_t kn = 0;
+      double a[D + 1];
+      a[0] = 1.0;
+#pragma unroll
+      for (int l = 0; l < D; ++l) {
+        const int c = locate_g<EQ>(P, G.edge, Xn[l]);
+        kn = kn * (uint32_t)P.C + (uint32_t)c;
+        a[1 + l] = Xn[l] - G.cen[c];
+      }
+      const double* blk = P.table + ((size_t)(j + 1) * (size_t)P.K_pad + kn) * (size_t)KC::NBP;
+      double v = 0.0;
+#pragma unroll
+      for (int p = 0; p <= D; ++p) v = fma(__ldg(blk + p), a[p], v);
+      yv = trunc_L(v, P.C_y);
+#pragma unroll 1
+      for (int l = 0; l < Q; ++l) {
+        double w = 0.0;
+#pragma unroll
+        for (int p = 0; p <= D; ++p) w = fma(__ldg(blk + KC::NH + l * KC::N1 + p), a[p], w);
+        zn[l] = trunc_L(w, P.C_z);
+      }
+    } else {
+      yv = g_eval<D>(P, Xn);                       // y_N := g
+#pragma unroll
+      for (int l = 0; l < Q; ++l) zn[l] = 0.0;
+    }
+    if (j == i) Y1 = yv;
+    else acc = acc + f_user<D, Q>(P, tj, X, yv, zc) * P.dt;   // f_j(x_j, y_{j+1}(x_{j+1}), z_j(x_j)) dt
+#pragma unroll
+    for (int l = 0; l < Q; ++l) zc[l] = zn[l];
+#pragma unroll
+    for (int l = 0; l < D; ++l) X[l] = Xn[l];
+  }
+  Bout = yv + acc;
+  Y1out = Y1;
+}
+#endif
 
 // Cholesky of the symmetric n x n matrix in A (full storage), lower factor in
 // place. Returns 1 iff positive definite with min diag(L) >= 1e-10 max diag(L)
@@ -355,7 +434,11 @@ step_kernel(const DevProblem P, const int i, const int64_t k_begin, const int64_
       if (m < M) {
         double* row = sRows + tid * KC::ROW;
         double Bv, Y1;
+#if SRMDP_USER_F
+        simulate_path_user<D, Q, EQ>(P, G, cc, i, k, (uint32_t)m, row, Bv, Y1);
+#else
         simulate_path<D, Q, EQ>(P, G, cc, i, k, (uint32_t)m, row, Bv, Y1);
+#endif
         const double sc = Bv * P.inv_dt;
 #pragma unroll
         for (int l = 0; l < Q; ++l) row[1 + D + l] = row[1 + D + l] * sc;   // S_{Z,i} = S_{Y,i+1} dW_i / dt
@@ -518,6 +601,19 @@ step_kernel(const DevProblem P, const int i, const int64_t k_begin, const int64_
 #pragma unroll
         for (int l = 0; l < D; ++l) a[1 + l] = x[l] - G.cen[cc[l]];
       }
+#if SRMDP_USER_F
+      // user driver: f(t_i, x_i, Y1, z_i(x_i)) with the full truncated z_i of
+      // the fresh blocks; x_i regenerated exactly (same bits as pass 1)
+      double xi[D], zi[Q];
+      start_point<D, EQ>(P, G, cc, i, k, (uint32_t)m, xi);
+      for (int l = 0; l < Q; ++l) {
+        double v = 0.0;
+#pragma unroll
+        for (int p = 0; p < KC::N1; ++p) v = fma(sBZ[l * KC::N1 + p], a[p], v);
+        zi[l] = trunc_L(v, P.C_z);
+      }
+      const double Sm = BYs[m] + f_user<D, Q>(P, (double)i * dt, xi, BYs[M + m], zi) * dt;
+#else
       // z_i(x_i) through the certificate of the fresh blocks (as eval_block)
       double zl = 0.0;
       int hm = 0x3ff00000;
@@ -535,6 +631,7 @@ step_kernel(const DevProblem P, const int i, const int64_t k_begin, const int64_
         }
       }
       const double Sm = BYs[m] + f_eval(P, BYs[M + m], zl) * dt;
+#endif
 #pragma unroll
       for (int p = 0; p < KC::N1; ++p) ry[p] = fma(a[p], Sm, ry[p]);
     }

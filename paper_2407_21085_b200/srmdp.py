@@ -16,16 +16,17 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("SRMDP_LIB") or os.path.join(_HERE, "libsrmdp_b200.so")   # override: A/B builds
 
-DYN = {"bm": 0, "gbm": 1, "affine": 2, "gbm_exact": 3}
-FKIND = {"zero": 0, "linear": 1, "paper": 2}
-GKIND = {"affine": 0, "paper": 1}
+DYN = {"bm": 0, "gbm": 1, "affine": 2, "gbm_exact": 3, "user": 4}
+FKIND = {"zero": 0, "linear": 1, "paper": 2, "user": 3}
+GKIND = {"affine": 0, "paper": 1, "user": 2}
 FLAG_NO_GRAPH = 1
 FLAG_TIME_KERNELS = 2
 FLAG_FORCE_NCCL = 4
 FLAG_LOOPBACK = 8
+FLAG_JIT = 16
 
 STATUS = {0: "SRMDP_OK", -1: "SRMDP_E_ARG", -2: "SRMDP_E_PRECOND", -3: "SRMDP_E_STATE", -4: "SRMDP_E_CUDA",
-          -5: "SRMDP_E_NCCL", -6: "SRMDP_E_NOMEM", -7: "SRMDP_E_UNSUPPORTED"}
+          -5: "SRMDP_E_NCCL", -6: "SRMDP_E_NOMEM", -7: "SRMDP_E_UNSUPPORTED", -8: "SRMDP_E_JIT"}
 
 
 class SrmdpError(RuntimeError):
@@ -51,6 +52,8 @@ class srmdp_config(ctypes.Structure):
         ("device", ctypes.c_int), ("stream", ctypes.c_void_p), ("flags", ctypes.c_int),
         ("lp0", ctypes.c_int),
         ("grid", ctypes.c_int),
+        ("user_src", ctypes.c_char_p), ("user_params", ctypes.POINTER(ctypes.c_double)),
+        ("n_user_params", ctypes.c_int),
     ]
 
 
@@ -90,6 +93,8 @@ SIGNATURES = {
     "srmdp_stats": (ctypes.c_int, [_H, ctypes.POINTER(srmdp_stats_t)]),
     "srmdp_shard_plan": (ctypes.c_int, [ctypes.c_int64, ctypes.c_int, ctypes.c_int, _P64]),
     "srmdp_build_info": (ctypes.c_char_p, []),
+    "srmdp_jit_check": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                       ctypes.c_char_p, ctypes.c_char_p, ctypes.c_size_t]),
     "srmdp_debug_trace": (ctypes.c_int, [_H, ctypes.c_int, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, _PD, _P64, _PD]),
     "srmdp_debug_detmath": (ctypes.c_int, [ctypes.c_int, ctypes.c_size_t, _PD, _PD, _PD]),
     "srmdp_debug_philox": (ctypes.c_int, [ctypes.c_size_t, _PU32, _PU32, _PU32]),
@@ -130,6 +135,17 @@ def srmdp_last_error(h=None) -> str:
     return library().srmdp_last_error(h).decode()
 
 
+def srmdp_jit_check(d: int, q: int, dyn: str, f: str, g: str, user_src: str | None = None):
+    """NVRTC-compile the kernels of a user problem without a GPU. Returns
+    (ok, log); see srmdp.h."""
+    buf = ctypes.create_string_buffer(1 << 16)
+    st = library().srmdp_jit_check(d, q, DYN[dyn], FKIND[f], GKIND[g],
+                                   user_src.encode() if user_src is not None else None, buf, len(buf))
+    if st == -1:
+        raise SrmdpError(st, "d, q must be in 1..32")
+    return st == 0, buf.value.decode()
+
+
 def srmdp_shard_plan(K: int, world: int, rank: int):
     out = (ctypes.c_int64 * 4)()
     _check(library().srmdp_shard_plan(K, world, rank, out))
@@ -168,6 +184,14 @@ def config_from_workload(w: dict, rank: int = 0, world: int = 1, device: int = 0
     cfg.rank, cfg.world, cfg.device, cfg.flags = rank, world, device, flags
     cfg.lp0 = 1 if w.get("basis", "lp1") == "lp0" else 0
     cfg.grid = 1 if w.get("grid", "uniform") == "equiprobable" else 0
+    if w.get("user_src") is not None:          # user problem (srmdp.h, SRMDP_*_USER)
+        src = ctypes.create_string_buffer(w["user_src"].encode())
+        keep.append(src)
+        cfg.user_src = ctypes.cast(src, ctypes.c_char_p)
+    up = np.ascontiguousarray(np.asarray(w.get("user_params", []), dtype=np.float64).ravel())
+    keep.append(up)
+    cfg.n_user_params = int(up.size)
+    cfg.user_params = _dp(up) if up.size else None
     if nccl_id is not None:
         idbuf = ctypes.create_string_buffer(bytes(nccl_id), 128)
         keep.append(idbuf)
