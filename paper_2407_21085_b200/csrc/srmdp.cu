@@ -13,6 +13,8 @@
 
 #include <chrono>
 #include <cmath>
+#include <map>
+#include <mutex>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -298,6 +300,44 @@ static srmdp_status cuda_fail(const srmdp_t* h, cudaError_t e, const char* what)
   return (e == cudaErrorMemoryAllocation) ? SRMDP_E_NOMEM : SRMDP_E_CUDA;
 }
 
+// Device memory of the handles comes from one process-wide stream-ordered
+// pool per device that keeps its pages (release threshold = max): creating and
+// destroying handles (one solve per request in a serving loop, the e2e bench)
+// reuses memory instead of cudaMalloc / cudaFree, whose unmapping of the
+// 240 MB cfg4 table took up to ~0.4 s (tools/e2e_breakdown.py).
+static cudaError_t device_pool(int dev, cudaMemPool_t* out) {
+  static std::mutex mu;
+  static std::map<int, cudaMemPool_t> pools;
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = pools.find(dev);
+  if (it != pools.end()) { *out = it->second; return cudaSuccess; }
+  cudaMemPoolProps props{};
+  props.allocType = cudaMemAllocationTypePinned;
+  props.location.type = cudaMemLocationTypeDevice;
+  props.location.id = dev;
+  cudaMemPool_t pool;
+  cudaError_t e = cudaMemPoolCreate(&pool, &props);
+  if (e != cudaSuccess) return e;
+  uint64_t keep = ~0ull;
+  e = cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  if (e != cudaSuccess) return e;
+  pools[dev] = pool;
+  *out = pool;
+  return cudaSuccess;
+}
+
+template <typename T>
+static cudaError_t dalloc(const srmdp_t* h, T** p, size_t bytes) {
+  cudaMemPool_t pool;
+  cudaError_t e = device_pool(h->cfg.device, &pool);
+  if (e != cudaSuccess) return e;
+  return cudaMallocFromPoolAsync((void**)p, bytes < 16 ? 16 : bytes, pool, h->stream);
+}
+
+static void dfree(const srmdp_t* h, void* p) {
+  if (p) cudaFreeAsync(p, h->stream);
+}
+
 #define CK(h, call, what)                                  \
   do {                                                     \
     cudaError_t _e = (call);                               \
@@ -523,21 +563,26 @@ extern "C" srmdp_status srmdp_create(const srmdp_config* cfg, srmdp_t** out) {
     if (e != cudaSuccess) { cuda_fail(h, e, "cudaStreamCreate"); return fail(SRMDP_E_CUDA); }
     h->own_stream = true;
   }
-  cudaDeviceProp prop;
-  cudaGetDeviceProperties(&prop, cfg->device);
-  h->sms = prop.multiProcessorCount;
+  e = cudaDeviceGetAttribute(&h->sms, cudaDevAttrMultiProcessorCount, cfg->device);
+  if (e != cudaSuccess) { cuda_fail(h, e, "device attribute"); return fail(SRMDP_E_CUDA); }
 
   const size_t table_bytes = (size_t)h->N * h->K_pad * h->B_pad * sizeof(double);
   std::vector<double> tabs = grid_tables(h->C, cfg->L, cfg->mu, cfg->grid != 0);
-  if ((e = cudaMalloc(&h->d_table, table_bytes)) != cudaSuccess) { cuda_fail(h, e, "table alloc"); return fail(SRMDP_E_NOMEM); }
-  if ((e = cudaMalloc(&h->d_params, h->params.size() * sizeof(double))) != cudaSuccess ||
-      (e = cudaMalloc(&h->d_tabs, tabs.size() * sizeof(double))) != cudaSuccess ||
-      (e = cudaMalloc(&h->d_lp0, sizeof(unsigned long long))) != cudaSuccess) {
+  if ((e = dalloc(h, &h->d_table, table_bytes)) != cudaSuccess) { cuda_fail(h, e, "table alloc"); return fail(SRMDP_E_NOMEM); }
+  if ((e = dalloc(h, &h->d_params, h->params.size() * sizeof(double))) != cudaSuccess ||
+      (e = dalloc(h, &h->d_tabs, tabs.size() * sizeof(double))) != cudaSuccess ||
+      (e = dalloc(h, &h->d_lp0, sizeof(unsigned long long))) != cudaSuccess) {
     cuda_fail(h, e, "alloc");
     return fail(SRMDP_E_NOMEM);
   }
-  cudaMemcpy(h->d_params, h->params.data(), h->params.size() * sizeof(double), cudaMemcpyHostToDevice);
-  cudaMemcpy(h->d_tabs, tabs.data(), tabs.size() * sizeof(double), cudaMemcpyHostToDevice);
+  if ((e = cudaMemcpyAsync(h->d_params, h->params.data(), h->params.size() * sizeof(double), cudaMemcpyHostToDevice,
+                           h->stream)) != cudaSuccess ||
+      (e = cudaMemcpyAsync(h->d_tabs, tabs.data(), tabs.size() * sizeof(double), cudaMemcpyHostToDevice,
+                           h->stream)) != cudaSuccess ||
+      (e = cudaStreamSynchronize(h->stream)) != cudaSuccess) {   // pageable sources: complete before return
+    cuda_fail(h, e, "upload");
+    return fail(SRMDP_E_CUDA);
+  }
   h->tabs = tabs;
 
   // launch configuration: persistent CTAs; the pass-2 records go to a per-CTA
@@ -552,7 +597,7 @@ extern "C" srmdp_status srmdp_create(const srmdp_config* cfg, srmdp_t** out) {
   const int64_t nk = (cfg->flags & SRMDP_FLAG_LOOPBACK) ? h->chunk : h->k_end - h->k_begin;
   const int64_t full = (int64_t)h->ctas * h->sms;
   h->grid = (int)(nk < full ? (nk > 0 ? nk : 1) : full);
-  if ((e = cudaMalloc(&h->d_scratch, (size_t)h->grid * h->M * scratch_stride(h->d) * sizeof(double))) != cudaSuccess) {
+  if ((e = dalloc(h, &h->d_scratch, (size_t)h->grid * h->M * scratch_stride(h->d) * sizeof(double))) != cudaSuccess) {
     cuda_fail(h, e, "scratch alloc");
     return fail(SRMDP_E_NOMEM);
   }
@@ -738,10 +783,10 @@ extern "C" srmdp_status srmdp_coeffs(const srmdp_t* h, int i, int basis, double*
 static srmdp_status ensure_io(const srmdp_t* hc, size_t bytes) {
   srmdp_t* h = const_cast<srmdp_t*>(hc);
   if (h->io_cap >= bytes) return SRMDP_OK;
-  if (h->d_io) cudaFree(h->d_io);
+  dfree(h, h->d_io);
   h->d_io = nullptr;
   h->io_cap = 0;
-  CK(h, cudaMalloc(&h->d_io, bytes), "io alloc");
+  CK(h, dalloc(h, &h->d_io, bytes), "io alloc");
   h->io_cap = bytes;
   return SRMDP_OK;
 }
@@ -888,12 +933,15 @@ extern "C" void srmdp_destroy(srmdp_t* h) {
   if (h->graph) cudaGraphExecDestroy(h->graph);
   for (auto& e : h->ev) cudaEventDestroy(e);
   if (h->comm && nccl().ok) nccl().CommDestroy(h->comm);
-  cudaFree(h->d_table);
-  cudaFree(h->d_params);
-  cudaFree(h->d_tabs);
-  cudaFree(h->d_scratch);
-  cudaFree(h->d_lp0);
-  cudaFree(h->d_io);
+  if (h->stream) {
+    dfree(h, h->d_table);
+    dfree(h, h->d_params);
+    dfree(h, h->d_tabs);
+    dfree(h, h->d_scratch);
+    dfree(h, h->d_lp0);
+    dfree(h, h->d_io);
+    cudaStreamSynchronize(h->stream);
+  }
   if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
   delete h;
 }
