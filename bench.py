@@ -192,7 +192,9 @@ def config_block(w, args):
     return {"workload": w["name"], "d": w["d"], "q": w["q"], "N": w["N"], "cells_per_dim": w["C"],
             "K": w["C"] ** w["d"], "M": w["M"], "problem": "PAPER.md §5.1 benchmark (X=W, mu=1, T=1, L=6.5)"
             if w["f"] == "paper" else w["name"], "path_steps_per_solve": workloads.path_steps(w),
-            "parallelism": "cells sharded over %d GPU(s), ncclAllGather per time step" % args.gpus,
+            "parallelism": "cells sharded over %d GPU(s), %s per time step" % (
+                args.gpus, "fused NVLink-store exchange" if getattr(args, "exchange", "nccl") == "p2p"
+                else "ncclAllGather"),
             "l2": "flushed (256 MB write) before every timed solve"}
 
 
@@ -206,6 +208,9 @@ def main():
     ap.add_argument("--M", type=int, default=None)
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--exchange", default="nccl", choices=["nccl", "p2p"],
+                    help="per-step slice exchange for N > 1: in-place ncclAllGather (default) or the fused "
+                         "NVLink store epilogue (SRMDP_FLAG_P2P_EXCHANGE)")
     ap.add_argument("--ref-path-steps", type=float, default=2.0e8)
     args = ap.parse_args()
 
@@ -248,8 +253,9 @@ def main():
         if world > 1:
             dist.barrier()
 
+    xflag = srmdp.FLAG_P2P_EXCHANGE if args.exchange == "p2p" else 0
     solver = srmdp.Solver(w, rank=rank, world=world, device=local, stream=stream.cuda_stream,
-                          flags=srmdp.FLAG_TIME_KERNELS, nccl_id=nccl_id)
+                          flags=srmdp.FLAG_TIME_KERNELS | xflag, nccl_id=nccl_id)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
 
     for _ in range(args.warmup):
@@ -300,7 +306,7 @@ def main():
         barrier()
         t0 = time.perf_counter()
         sv = srmdp.Solver(w, rank=rank, world=world, device=local, stream=stream.cuda_stream,
-                          nccl_id=fresh_nccl_id())
+                          flags=xflag, nccl_id=fresh_nccl_id())
         sv.solve()
         for i in range(w["N"]):
             sv.coeffs(i, 1, hnp[i])
@@ -333,7 +339,8 @@ def main():
             "e2e": {"value": path_steps * args.steps / e2e_s, "unit": "path-steps/s",
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "calls": "srmdp_create+srmdp_solve+srmdp_coeffs(all i, pinned host)+srmdp_destroy"},
-            "gpu_launches": launches_per_solve * args.steps,
+            # step kernels + (fused exchange) the epoch / entry-barrier kernels and a signal + wait per slice
+            "gpu_launches": (launches_per_solve + ((3 + 2 * w["N"]) if args.exchange == "p2p" else 0)) * args.steps,
             "clocks": clk.summary(),
             "lp0_fallbacks": st["lp0_fallbacks"],
             "launch": {"grid": st["grid"], "block": st["block"], "smem_bytes": st["smem_bytes"],

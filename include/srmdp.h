@@ -109,6 +109,12 @@ typedef struct {
                                      shards one after another on the same table, no NCCL (tests sharding
                                      and padding on one GPU; `rank` is ignored) */
 #define SRMDP_FLAG_JIT         16 /* build the kernels with NVRTC even when (d, q) is compiled in */
+#define SRMDP_FLAG_P2P_EXCHANGE 32 /* fused exchange instead of ncclAllGather: every step kernel's
+                                     epilogue stores each block into all ranks' tables over NVLink
+                                     (CUDA IPC mappings, world <= 8, one node); per-slice release /
+                                     acquire flags at system scope order the stores against the next
+                                     step's reads. NCCL is still used once, at create, to exchange
+                                     the IPC handles (world > 1). */
 
 typedef struct {
   int d, q, N;          /* state dim, Brownian dim, time steps */

@@ -1,0 +1,53 @@
+// exchange_kernels.cuh — cross-GPU completion flags of the fused exchange
+// (SRMDP_FLAG_P2P_EXCHANGE, srmdp.cu). The step kernel's epilogue stores each
+// coefficient block into every rank's table (peer pointers opened through
+// CUDA IPC); these kernels order those stores against the next step's reads.
+//
+// flags: every rank owns a uint32 array [N + 1][world] (IPC-shared). Slot i
+// (0 <= i < N) says "rank r has written all its blocks of slice i into my
+// table"; slot N is the entry barrier of a solve (no rank writes into a peer's
+// table before that peer has entered the same solve). Values are the solve
+// epoch, so flags never need resetting. Release / acquire at system scope.
+// Non-template: included by srmdp.cu only.
+#pragma once
+#include "detmath.cuh"
+
+namespace srk {
+
+constexpr int kMaxRanks = 8;
+
+struct FlagPtrs {
+  unsigned* f[kMaxRanks];   // every rank's flag array (own included), as mapped here
+};
+
+__global__ void epoch_kernel(unsigned* epoch) { *epoch = *epoch + 1u; }
+
+// After the step kernel of slice `slot` (same stream): make this rank's
+// stores to the peers' tables visible, then publish the epoch in every
+// rank's flag array at [slot][rank].
+__global__ void exchange_signal_kernel(const FlagPtrs F, int world, int rank, int slot, const unsigned* epoch) {
+  const int r = threadIdx.x;
+  if (r >= world) return;
+  __threadfence_system();
+  const unsigned e = *epoch;
+  unsigned* p = F.f[r] + (size_t)slot * world + rank;
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(e) : "memory");
+}
+
+// Before anything reads slice `slot` (or, for the entry slot, before the
+// first peer store): wait until every rank has published this epoch.
+__global__ void exchange_wait_kernel(const unsigned* own, int world, int slot, const unsigned* epoch) {
+  const int r = threadIdx.x;
+  if (r >= world) return;
+  const unsigned e = *epoch;
+  const unsigned* p = own + (size_t)slot * world + r;
+  unsigned v;
+  for (;;) {
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    if ((int)(v - e) >= 0) break;
+    __nanosleep(200);
+  }
+  __threadfence_system();
+}
+
+}  // namespace srk

@@ -25,6 +25,7 @@
 #include "../../include/srmdp_debug.h"
 #include "aux_kernels.cuh"
 #include "debug_kernels.cuh"
+#include "exchange_kernels.cuh"
 #include "jit.h"
 #include "ops.h"
 
@@ -282,6 +283,14 @@ struct srmdp {
   cudaGraphExec_t graph = nullptr;
   ncclComm_t comm = nullptr;
   bool solved = false;
+  // fused exchange (SRMDP_FLAG_P2P_EXCHANGE)
+  bool p2p = false;
+  void* ipc_base = nullptr;          // cudaMalloc'd [table | flags], IPC-exported
+  size_t ipc_bytes = 0;
+  unsigned* d_flags = nullptr;       // own flags [N+1][world]
+  unsigned* d_epoch = nullptr;
+  FlagPtrs fptr{};
+  std::vector<void*> opened;         // peers' bases opened through IPC
   int launches_per_solve = 0;
   int valid_from = 0;          // slices valid_from .. N-1 are present (N: none)
   int graph_launches = 0;
@@ -324,6 +333,30 @@ static cudaError_t device_pool(int dev, cudaMemPool_t* out) {
   pools[dev] = pool;
   *out = pool;
   return cudaSuccess;
+}
+
+// IPC-exportable allocations of the fused exchange ([table | flags],
+// cudaMalloc: pool memory cannot be exported with cudaIpcGetMemHandle) are
+// kept the same way: freed blocks are cached per (device, size) and reused.
+static std::mutex g_ipc_mu;
+static std::multimap<std::pair<int, size_t>, void*> g_ipc_free;
+
+static cudaError_t ipc_alloc(int dev, void** p, size_t bytes) {
+  {
+    std::lock_guard<std::mutex> lock(g_ipc_mu);
+    auto it = g_ipc_free.find({dev, bytes});
+    if (it != g_ipc_free.end()) {
+      *p = it->second;
+      g_ipc_free.erase(it);
+      return cudaSuccess;
+    }
+  }
+  return cudaMalloc(p, bytes);
+}
+
+static void ipc_release(int dev, void* p, size_t bytes) {
+  std::lock_guard<std::mutex> lock(g_ipc_mu);
+  g_ipc_free.insert({{dev, bytes}, p});
 }
 
 template <typename T>
@@ -393,6 +426,8 @@ static srmdp_status validate(const srmdp_config* c, std::string& err) {
   if (((c->world > 1 && !loopback) || (c->flags & SRMDP_FLAG_FORCE_NCCL)) && !c->nccl_unique_id)
     return bad(SRMDP_E_ARG, "the NCCL exchange needs nccl_unique_id");
   if (loopback && (c->flags & SRMDP_FLAG_FORCE_NCCL)) return bad(SRMDP_E_ARG, "LOOPBACK and FORCE_NCCL exclude each other");
+  if ((c->flags & SRMDP_FLAG_P2P_EXCHANGE) && (loopback || c->world > kMaxRanks))
+    return bad(SRMDP_E_ARG, "P2P_EXCHANGE needs world <= 8 and excludes LOOPBACK");
   if (c->dyn.kind < 0 || c->dyn.kind > 4 || c->driver.kind < 0 || c->driver.kind > 3 || c->terminal.kind < 0 ||
       c->terminal.kind > 2)
     return bad(SRMDP_E_ARG, "unknown problem family kind");
@@ -467,6 +502,14 @@ static srmdp_status enqueue_sweep(srmdp_t* h, int i_hi, int i_lo) {
   const int64_t nk = h->k_end - h->k_begin;
   const bool loopback = h->cfg.flags & SRMDP_FLAG_LOOPBACK;
   h->launches_per_solve = 0;
+  if (h->p2p) {
+    // new epoch; entry barrier: no rank stores into a peer's table before
+    // that peer has entered this sweep (slot N)
+    epoch_kernel<<<1, 1, 0, h->stream>>>(h->d_epoch);
+    exchange_signal_kernel<<<1, kMaxRanks, 0, h->stream>>>(h->fptr, h->cfg.world, h->cfg.rank, h->N, h->d_epoch);
+    exchange_wait_kernel<<<1, kMaxRanks, 0, h->stream>>>(h->d_flags, h->cfg.world, h->N, h->d_epoch);
+    CK(h, cudaGetLastError(), "exchange entry barrier");
+  }
   for (int i = i_hi; i >= i_lo; --i) {
     if (timed) CK(h, record_event(h, h->ev[2 * i]), "event");
     if (loopback) {
@@ -484,7 +527,12 @@ static srmdp_status enqueue_sweep(srmdp_t* h, int i_hi, int i_lo) {
     }
     CK(h, cudaGetLastError(), "step kernel launch");
     if (timed) CK(h, record_event(h, h->ev[2 * i + 1]), "event");
-    if (h->comm) {
+    if (h->p2p) {
+      // blocks of slice i are in every table once all ranks have signalled
+      exchange_signal_kernel<<<1, kMaxRanks, 0, h->stream>>>(h->fptr, h->cfg.world, h->cfg.rank, i, h->d_epoch);
+      exchange_wait_kernel<<<1, kMaxRanks, 0, h->stream>>>(h->d_flags, h->cfg.world, i, h->d_epoch);
+      CK(h, cudaGetLastError(), "exchange flags");
+    } else if (h->comm) {
       double* slice = h->d_table + (size_t)i * h->K_pad * h->B_pad;
       const size_t cnt = (size_t)h->chunk * h->B_pad;
       ncclResult_t r = nccl().AllGather(slice + (size_t)h->cfg.rank * cnt, slice, cnt, ncclDouble, h->comm, h->stream);
@@ -568,7 +616,25 @@ extern "C" srmdp_status srmdp_create(const srmdp_config* cfg, srmdp_t** out) {
 
   const size_t table_bytes = (size_t)h->N * h->K_pad * h->B_pad * sizeof(double);
   std::vector<double> tabs = grid_tables(h->C, cfg->L, cfg->mu, cfg->grid != 0);
-  if ((e = dalloc(h, &h->d_table, table_bytes)) != cudaSuccess) { cuda_fail(h, e, "table alloc"); return fail(SRMDP_E_NOMEM); }
+  h->p2p = cfg->flags & SRMDP_FLAG_P2P_EXCHANGE;
+  const size_t flags_off = (table_bytes + 255) & ~(size_t)255;
+  const size_t flags_bytes = (size_t)(h->N + 1) * cfg->world * sizeof(unsigned);
+  if (h->p2p) {   // IPC-exportable allocation: [table | flags]
+    h->ipc_bytes = flags_off + flags_bytes;
+    if ((e = ipc_alloc(cfg->device, &h->ipc_base, h->ipc_bytes)) != cudaSuccess ||
+        (e = cudaMemsetAsync((char*)h->ipc_base + flags_off, 0, flags_bytes, h->stream)) != cudaSuccess ||
+        (e = dalloc(h, &h->d_epoch, sizeof(unsigned))) != cudaSuccess ||
+        (e = cudaMemsetAsync(h->d_epoch, 0, sizeof(unsigned), h->stream)) != cudaSuccess) {
+      cuda_fail(h, e, "p2p table alloc");
+      return fail(SRMDP_E_NOMEM);
+    }
+    h->d_table = (double*)h->ipc_base;
+    h->d_flags = (unsigned*)((char*)h->ipc_base + flags_off);
+    h->fptr.f[cfg->rank] = h->d_flags;
+  } else if ((e = dalloc(h, &h->d_table, table_bytes)) != cudaSuccess) {
+    cuda_fail(h, e, "table alloc");
+    return fail(SRMDP_E_NOMEM);
+  }
   if ((e = dalloc(h, &h->d_params, h->params.size() * sizeof(double))) != cudaSuccess ||
       (e = dalloc(h, &h->d_tabs, tabs.size() * sizeof(double))) != cudaSuccess ||
       (e = dalloc(h, &h->d_lp0, sizeof(unsigned long long))) != cudaSuccess) {
@@ -647,6 +713,39 @@ extern "C" srmdp_status srmdp_create(const srmdp_config* cfg, srmdp_t** out) {
     memcpy(&id, cfg->nccl_unique_id, sizeof(id));
     ncclResult_t r = api.CommInitRank(&h->comm, cfg->world, id, cfg->rank);
     if (r != ncclSuccess) { h->err = std::string("ncclCommInitRank: ") + api.GetErrorString(r); return fail(SRMDP_E_NCCL); }
+  }
+  if (h->p2p && cfg->world > 1) {
+    // exchange the IPC handles of [table | flags] over the communicator, open the peers'
+    if (!h->comm) { h->err = "P2P_EXCHANGE with world > 1 needs nccl_unique_id"; return fail(SRMDP_E_ARG); }
+    cudaIpcMemHandle_t mine;
+    if ((e = cudaIpcGetMemHandle(&mine, h->ipc_base)) != cudaSuccess) { cuda_fail(h, e, "ipc handle"); return fail(SRMDP_E_CUDA); }
+    const size_t hb = sizeof(cudaIpcMemHandle_t);
+    std::vector<cudaIpcMemHandle_t> all(cfg->world);
+    char* dbuf = nullptr;
+    if ((e = dalloc(h, &dbuf, hb * (cfg->world + 1))) != cudaSuccess ||
+        (e = cudaMemcpyAsync(dbuf, &mine, hb, cudaMemcpyHostToDevice, h->stream)) != cudaSuccess) {
+      cuda_fail(h, e, "ipc exchange");
+      return fail(SRMDP_E_CUDA);
+    }
+    ncclResult_t r = nccl().AllGather(dbuf, dbuf + hb, hb, ncclChar, h->comm, h->stream);
+    if (r != ncclSuccess) { h->err = std::string("ncclAllGather (ipc handles): ") + nccl().GetErrorString(r); return fail(SRMDP_E_NCCL); }
+    e = cudaMemcpyAsync(all.data(), dbuf + hb, hb * cfg->world, cudaMemcpyDeviceToHost, h->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
+    dfree(h, dbuf);
+    if (e != cudaSuccess) { cuda_fail(h, e, "ipc exchange"); return fail(SRMDP_E_CUDA); }
+    int np = 0;
+    for (int r2 = 0; r2 < cfg->world; ++r2) {
+      if (r2 == cfg->rank) continue;
+      void* base = nullptr;
+      if ((e = cudaIpcOpenMemHandle(&base, all[r2], cudaIpcMemLazyEnablePeerAccess)) != cudaSuccess) {
+        cuda_fail(h, e, "cudaIpcOpenMemHandle (peers must share an NVLink domain)");
+        return fail(SRMDP_E_CUDA);
+      }
+      h->opened.push_back(base);
+      h->dp.peer_table[np++] = (double*)base;
+      h->fptr.f[r2] = (unsigned*)((char*)base + flags_off);
+    }
+    h->dp.n_peers = np;
   }
   h->valid_from = h->N;
   h->st.path_steps = (uint64_t)h->K * (uint64_t)h->M * (uint64_t)h->N * (uint64_t)(h->N + 1) / 2;
@@ -933,7 +1032,14 @@ extern "C" void srmdp_destroy(srmdp_t* h) {
   if (h->graph) cudaGraphExecDestroy(h->graph);
   for (auto& e : h->ev) cudaEventDestroy(e);
   if (h->comm && nccl().ok) nccl().CommDestroy(h->comm);
+  for (void* b : h->opened) cudaIpcCloseMemHandle(b);
+  if (h->ipc_base) {
+    if (h->stream) cudaStreamSynchronize(h->stream);
+    ipc_release(h->cfg.device, h->ipc_base, h->ipc_bytes);
+    h->d_table = nullptr;
+  }
   if (h->stream) {
+    dfree(h, h->d_epoch);
     dfree(h, h->d_table);
     dfree(h, h->d_params);
     dfree(h, h->d_tabs);

@@ -667,7 +667,11 @@ step_kernel(const DevProblem P, const int i, const int64_t k_begin, const int64_
       else if (b == 2 * KC::N1) v = sS[0];
       else if (b >= KC::NH && b < KC::NH + KC::NZ) v = sBZ[b - KC::NH];
       dst[b] = v;
+      // fused exchange: the same block into every peer's replica (NVLink
+      // stores, coalesced per block); made visible by exchange_signal_kernel
+      for (int r = 0; r < P.n_peers; ++r) P.peer_table[r][(dst - P.table) + b] = v;
     }
+    if (P.n_peers) __threadfence_system();   // peer stores ordered before the signal kernel's release
     __syncthreads();
   }
 }
