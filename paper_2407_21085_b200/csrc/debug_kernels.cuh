@@ -12,6 +12,7 @@ __global__ void detmath_kernel(const int op, const int64_t n, const double* __re
   DetTabs T;
   T.logt = reinterpret_cast<const double2*>(det);
   T.sct = reinterpret_cast<const double2*>(det + 256);
+  T.stride = 1;
   if (op == 0) {
     o0[t] = dm_log(in[t], T);
   } else {

@@ -31,7 +31,7 @@ constexpr int kThreads = 256;
 // functions so the host sizes NVRTC-built kernels with the same formula.
 __host__ __device__ constexpr int row_stride(int d, int q) { return (1 + d + q) | 1; }
 __host__ __device__ constexpr size_t step_smem_bytes(int d, int q, int C) {
-  return sizeof(double) * (size_t)((tabs_len(C) + kThreads * row_stride(d, q) + 1) & ~1);
+  return sizeof(double) * (size_t)((smem_tabs_len(d, C) + kThreads * row_stride(d, q) + 1) & ~1);
 }
 
 template <int D, int Q>
@@ -84,7 +84,7 @@ struct SmemLayout {
                                    : kThreads) + 1) & ~1;
   static constexpr int SOLVE = KC::N1 * KC::N1 + 2 * KC::NZ + 2 * KC::N1 + (kThreads / 32) * KC::N1 + 2 + KC::N1 + 2;
   static_assert(RED + SOLVE <= KC::ROWS * KC::ROW, "solve arrays must fit in the row tile");
-  __host__ __device__ static int tabs(int C) { return tabs_len(C); }
+  __host__ __device__ static int tabs(int C) { return smem_tabs_len(D, C); }
   __host__ __device__ static int rows(int C) { return tabs(C); }
   __host__ __device__ static int L(int C) { return rows(C) + RED; }
   __host__ __device__ static int RZ(int C) { return L(C) + KC::N1 * KC::N1; }
@@ -368,7 +368,8 @@ step_kernel(const DevProblem P, const int i, const int64_t k_begin, const int64_
   const int C = P.C;
   const int tid = threadIdx.x;
   const int warp = tid >> 5, gid = (tid & 31) >> 2, tig = tid & 3;   // MMA fragment coordinates
-  const Grid G = make_grid(sm, C);
+  constexpr int TC = tab_copies(D);
+  const Grid G = make_grid_smem<TC>(sm, C);
   double* sRows = sm + SL::rows(C);
   double* sL = sm + SL::L(C);
   double* sRZ = sm + SL::RZ(C);
@@ -382,7 +383,13 @@ step_kernel(const DevProblem P, const int i, const int64_t k_begin, const int64_
   constexpr int SB = scratch_stride(D);
   double* BYs = P.by_scratch + (size_t)blockIdx.x * (size_t)P.M * SB;   // this CTA's pass-2 records
 
-  for (int t = tid; t < tabs_len(C); t += kThreads) sm[t] = P.tabs[t];
+  {   // grid tables, then the detmath tables replicated entry by entry (DetTabs)
+    const int off = tabs_det_off(C);
+    for (int t = tid; t < off; t += kThreads) sm[t] = P.tabs[t];
+    const double2* src = reinterpret_cast<const double2*>(P.tabs + off);
+    double2* dst = reinterpret_cast<double2*>(sm + off);
+    for (int t = tid; t < 256 * TC; t += kThreads) dst[t] = src[t / TC];
+  }
 
   // Owner-compute assignment (scalar reduction path): pair idx -> (entry e, row slice s).
   int cA[KC::NACC], cB[KC::NACC], rlo[KC::NACC], rhi[KC::NACC];
