@@ -25,13 +25,26 @@ namespace srk {
 
 constexpr int kThreads = 256;
 
+// Kernel variants (A/B builds: build.py -DNAME=VALUE)
+#ifndef SRMDP_TOUCH
+#define SRMDP_TOUCH 0     // sector-touch loads instead of prefetch.global.L1 (measured slower)
+#endif
+#ifndef SRMDP_LDG256
+#define SRMDP_LDG256 1    // 256-bit hot-line loads
+#endif
+#ifndef SRMDP_PREFETCH
+#define SRMDP_PREFETCH 1
+#endif
+
 // Row stride (doubles) of the shared-memory row tile [1 | x - r_k | S dW/dt]:
 // odd (spreads banks). Dynamic shared memory of the step kernel for (d, q, C):
 // the grid tables then the row tile (the solve arrays alias the tile). Plain
 // functions so the host sizes NVRTC-built kernels with the same formula.
 __host__ __device__ constexpr int row_stride(int d, int q) { return (1 + d + q) | 1; }
+// (+8 doubles: the MMA fragment loads of the last row read up to 7 padding
+// columns past the tile; they only feed discarded outputs)
 __host__ __device__ constexpr size_t step_smem_bytes(int d, int q, int C) {
-  return sizeof(double) * (size_t)((smem_tabs_len(d, C) + kThreads * row_stride(d, q) + 1) & ~1);
+  return sizeof(double) * (size_t)((smem_tabs_len(d, C) + kThreads * row_stride(d, q) + 8 + 1) & ~1);
 }
 
 template <int D, int Q>
@@ -55,7 +68,13 @@ struct KCfg {
   static constexpr int NACC = (PAIRS + kThreads - 1) / kThreads;
   // Gram / Z right-hand sides by FP64 tensor-core MMA (mma.sync m8n8k4 f64):
   // C = V^T V over the rows V = [1 | x - r_k | S dW/dt] of a round
-  static constexpr bool USE_MMA = (D > 8);          // measured: +12% at d=19, -4% at d=6 (scalar owner-compute wins)
+#ifndef SRMDP_MMA_MIN_D
+#define SRMDP_MMA_MIN_D 4
+#endif
+  // FP64 MMA Gram: 4x fewer shared-memory wavefronts than the owner-compute
+  // fold (the L1 data pipe is the busiest unit once the gather uses 256-bit
+  // loads); measured d=19 +12%, d=6 +2.8% (scalar won at d=6 before LDG.256)
+  static constexpr bool USE_MMA = (D >= SRMDP_MMA_MIN_D);
   static constexpr int NCOL = 1 + D + Q;            // used columns of a row
   static constexpr int PB = (N1 + 7) / 8;           // 8-row blocks of C (p <= d)
   static constexpr int QB = (NCOL + 7) / 8;         // 8-column blocks of C
@@ -124,6 +143,24 @@ __device__ __forceinline__ void eval_block(const DevProblem& P, const double* __
   using KC = KCfg<D, Q>;
   constexpr int NHOT = 2 * KC::N1 + 1;
   double yv = 0.0, wv = 0.0, S = 0.0;
+#if SRMDP_LDG256
+  // 256-bit loads (LDG.E.ENL2.256, sm_100): half the L1 wavefronts of 128-bit
+  // loads for the divergent per-lane gather; blocks are 128-byte aligned
+#pragma unroll
+  for (int u = 0; u < (NHOT + 3) / 4; ++u) {
+    double v[4];
+    asm("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];"
+        : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3]) : "l"(blk + 4 * u));
+#pragma unroll
+    for (int h = 0; h < 4; ++h) {
+      const int e = 4 * u + h;
+      const double c = v[h];
+      if (e < KC::N1) yv = fma(c, a[e], yv);
+      else if (e < 2 * KC::N1) wv = fma(c, a[e - KC::N1], wv);
+      else if (e == 2 * KC::N1) S = c;
+    }
+  }
+#else
   const double2* b2 = reinterpret_cast<const double2*>(blk);
 #pragma unroll
   for (int u = 0; u < (NHOT + 1) / 2; ++u) {
@@ -137,6 +174,7 @@ __device__ __forceinline__ void eval_block(const DevProblem& P, const double* __
       else if (e == 2 * KC::N1) S = c;
     }
   }
+#endif
   y = trunc_L(yv, P.C_y);
   // conservative max(1, max_p |a_p|) from the high words (integer pipe)
   int hm = 0x3ff00000;
@@ -150,6 +188,9 @@ __device__ __forceinline__ void eval_block(const DevProblem& P, const double* __
 // L1 prefetch of a coefficient block (every 128-byte line it spans).
 template <int NHOT>
 __device__ __forceinline__ void prefetch_block(const double* blk) {
+#if !SRMDP_PREFETCH
+  return;
+#endif
 #pragma unroll
   for (int off = 0; off < NHOT * 8; off += 128) asm volatile("prefetch.global.L1 [%0];" ::"l"((const char*)blk + off));
 }
@@ -194,18 +235,35 @@ __device__ __forceinline__ void simulate_path(const DevProblem& P, const Grid& G
         c[l] = locate_g<EQ>(P, G.edge, Xn[l]);
         kn = kn * (uint32_t)P.C + (uint32_t)c[l];
       }
+#ifdef SRMDP_EXPERIMENT_GATHER_SELF   // timing experiment only (wrong results): every gather hits the start cell
+      kn = k;
+#endif
       const double* blk = P.table + ((size_t)(j + 1) * (size_t)P.K_pad + kn) * (size_t)KC::NBP;
+#if SRMDP_TOUCH
+      // pull the block's 32-byte sectors into L1 with one 4-byte load each;
+      // the dummy registers stay live (empty asm below) so the warp never
+      // waits on them -- the loads complete under the increments / Euler work
+      uint32_t t0, t1, t2, t3;
+      asm volatile("ld.global.ca.u32 %0, [%1];" : "=r"(t0) : "l"(blk));
+      asm volatile("ld.global.ca.u32 %0, [%1];" : "=r"(t1) : "l"(blk + 4));
+      asm volatile("ld.global.ca.u32 %0, [%1];" : "=r"(t2) : "l"(blk + 8));
+      asm volatile("ld.global.ca.u32 %0, [%1];" : "=r"(t3) : "l"(blk + 12));
+#else
       prefetch_block<2 * KC::N1 + 1>(blk);
+#endif
       double Xnn[D];
       {
         double dW[Q];
         brownian<Q>(P, G, i, j + 1, k, m, dW);   // increments of step j+1
         euler<D, Q>(P, (double)(j + 1) * P.dt, Xn, dW, Xnn);
       }
+#if SRMDP_TOUCH
+      asm volatile("" ::"r"(t0), "r"(t1), "r"(t2), "r"(t3));
+#endif
       double a[D + 1];
       a[0] = 1.0;
 #pragma unroll
-      for (int l = 0; l < D; ++l) a[1 + l] = Xn[l] - G.cen[c[l]];
+      for (int l = 0; l < D; ++l) a[1 + l] = Xn[l] - center_of<EQ>(P, G, c[l]);
       eval_block<D, Q>(P, blk, a, yv, zn);       // y_{j+1}(x_{j+1}), z_{j+1}(x_{j+1})
 #pragma unroll
       for (int l = 0; l < D; ++l) Xn[l] = Xnn[l];
