@@ -33,7 +33,7 @@ constexpr int kThreads = 256;
 #define SRMDP_LDG256 1    // 256-bit hot-line loads
 #endif
 #ifndef SRMDP_PREFETCH
-#define SRMDP_PREFETCH 1
+#define SRMDP_PREFETCH 0  // prefetch.global.L1 of the next hot line: measured -1.2% with the 256-bit loads
 #endif
 
 // Row stride (doubles) of the shared-memory row tile [1 | x - r_k | S dW/dt]:
@@ -199,10 +199,14 @@ __device__ __forceinline__ void prefetch_block(const double* blk) {
 // `row`). The design row (1, x_i - r_k) and dW_i are written to the row as soon
 // as they exist, so they do not stay in registers across the Euler chain.
 // Returns B = S_{Y,i+1}(x_i) = g(x_N) + sum_{j>i} f_j dt (eq. PsiM) and
-// Y1 = y_{i+1}(x_{i+1}). Software pipeline per step: the block of X_{j+1} is
-// located and prefetched into L1, the increments and Euler step of X_{j+2}
-// are computed (FP64-heavy, independent of the gather), then the block is
-// evaluated. (Two paths per thread for ILP measured slower: 2.43e10 vs 2.65e10.)
+// Y1 = y_{i+1}(x_{i+1}). Software pipeline per step: the cell of X_{j+1} is
+// located, the increments and Euler step of X_{j+2} are computed (FP64-heavy,
+// independent of the gather) while its 128-byte hot line is loaded with four
+// 256-bit loads, then the block is evaluated. The per-lane gather is
+// divergent (up to 32 lines per warp instruction), so the L1 data pipe, not
+// latency, is what it costs: 256-bit instead of 128-bit loads gained 7%, an
+// explicit L1 prefetch now loses 1%. (Two paths per thread for ILP measured
+// slower: 2.43e10 vs 2.65e10.)
 template <int D, int Q, bool EQ>
 __device__ __forceinline__ void simulate_path(const DevProblem& P, const Grid& G, const int (&cc)[D], int i,
                                               uint32_t k, uint32_t m, double* row, double& Bout, double& Y1out) {
