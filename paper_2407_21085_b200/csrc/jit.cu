@@ -36,6 +36,8 @@ struct NvrtcApi {
   decltype(&nvrtcGetLoweredName) GetLoweredName = nullptr;
   decltype(&nvrtcDestroyProgram) DestroyProgram = nullptr;
   decltype(&nvrtcGetErrorString) GetErrorString = nullptr;
+  decltype(&nvrtcVersion) Version = nullptr;
+  int major = 0, minor = 0;
 };
 
 NvrtcApi& nvrtc() {
@@ -44,9 +46,11 @@ NvrtcApi& nvrtc() {
   std::call_once(once, [] {
     void* h = nullptr;
     const char* env = getenv("SRMDP_NVRTC_LIB");
-    if (env) h = dlopen(env, RTLD_NOW | RTLD_GLOBAL);
-    if (!h) h = dlopen("libnvrtc.so.12", RTLD_NOW | RTLD_GLOBAL);
-    if (!h) h = dlopen("/usr/local/cuda/lib64/libnvrtc.so.12", RTLD_NOW | RTLD_GLOBAL);
+    // the toolkit's NVRTC first (the one the library was built with; torch may
+    // have mapped an older libnvrtc.so.12 under the same soname)
+    if (env) h = dlopen(env, RTLD_NOW | RTLD_LOCAL);
+    if (!h) h = dlopen("/usr/local/cuda/lib64/libnvrtc.so.12", RTLD_NOW | RTLD_LOCAL);
+    if (!h) h = dlopen("libnvrtc.so.12", RTLD_NOW | RTLD_LOCAL);
     if (!h) {
       api.err = std::string("cannot load libnvrtc.so.12: ") + dlerror();
       return;
@@ -62,7 +66,9 @@ NvrtcApi& nvrtc() {
     SYM(GetLoweredName);
     SYM(DestroyProgram);
     SYM(GetErrorString);
+    SYM(Version);
 #undef SYM
+    if (api.Version) api.Version(&api.major, &api.minor);
     api.ok = api.CreateProgram && api.AddNameExpression && api.CompileProgram && api.GetProgramLogSize &&
              api.GetProgramLog && api.GetCUBINSize && api.GetCUBIN && api.GetLoweredName && api.DestroyProgram &&
              api.GetErrorString;
@@ -116,8 +122,10 @@ static bool compile(const std::string& src, int d, int q, std::vector<char>& cub
   names[2] = "srk::eval_kernel<" + D + ", " + Q + ">";
   names[3] = "srk::trace_kernel<" + D + ", " + Q + ">";
   for (const std::string& n : names) api.AddNameExpression(prog, n.c_str());
+  // 256-bit loads (ld.global.nc.v4.f64) need NVRTC >= 12.9
+  const bool v256 = api.major > 12 || (api.major == 12 && api.minor >= 9);
   const char* opts[] = {"-arch=sm_100a", "-std=c++17", "--fmad=false", "-lineinfo", "-default-device",
-                        "-DSRMDP_JIT=1"};
+                        "-DSRMDP_JIT=1", v256 ? "-DSRMDP_LDG256=1" : "-DSRMDP_LDG256=0"};
   r = api.CompileProgram(prog, (int)(sizeof(opts) / sizeof(opts[0])), opts);
   size_t log_n = 0;
   api.GetProgramLogSize(prog, &log_n);
