@@ -32,6 +32,10 @@ constexpr int kThreads = 256;
 #ifndef SRMDP_LDG256
 #define SRMDP_LDG256 1    // 256-bit hot-line loads
 #endif
+#ifndef SRMDP_J_UNROLL
+#define SRMDP_J_UNROLL 2   // path-step loop unrolled by 2: X_{j+1} / X_{j+2} swap roles without register moves (+0.9%)
+#endif
+constexpr int kJUnroll = SRMDP_J_UNROLL;
 #ifndef SRMDP_PREFETCH
 #define SRMDP_PREFETCH 0  // prefetch.global.L1 of the next hot line: measured -1.2% with the 256-bit loads
 #endif
@@ -188,11 +192,10 @@ __device__ __forceinline__ void eval_block(const DevProblem& P, const double* __
 // L1 prefetch of a coefficient block (every 128-byte line it spans).
 template <int NHOT>
 __device__ __forceinline__ void prefetch_block(const double* blk) {
-#if !SRMDP_PREFETCH
-  return;
-#endif
+  if constexpr (SRMDP_PREFETCH != 0) {
 #pragma unroll
-  for (int off = 0; off < NHOT * 8; off += 128) asm volatile("prefetch.global.L1 [%0];" ::"l"((const char*)blk + off));
+    for (int off = 0; off < NHOT * 8; off += 128) asm volatile("prefetch.global.L1 [%0];" ::"l"((const char*)blk + off));
+  }
 }
 
 // One path of cloud (i,k), pass 1 (path m of this thread, shared-memory row
@@ -227,7 +230,7 @@ __device__ __forceinline__ void simulate_path(const DevProblem& P, const Grid& G
   }
   double acc = 0.0, zlin = 0.0, Y1 = 0.0, yv = 0.0;
   const int N = P.N;
-#pragma unroll 1
+#pragma unroll kJUnroll
   for (int j = i; j < N; ++j) {
     // Xn = X_{j+1}
     double zn = 0.0;
