@@ -40,6 +40,8 @@ SOLVE_CASES = [
     dict(workloads.user_nonlinear(d=3, q=3, N=4, C=4, M=200, seed=9), grid="equiprobable"),
     dict(workloads.user_nonlinear(d=2, q=2, N=4, C=4, M=200, seed=10), C_z_override=0.3, C_y_override=0.6),
     workloads.user_cfg2(N=5, C=6, M=128),
+    workloads.user_nonlinear(d=5, q=5, N=4, C=3, M=300, seed=16),    # MMA Gram path (d >= 4) with a user driver
+    workloads.user_nonlinear(d=6, q=2, N=3, C=2, M=257, seed=17),
     workloads.user_time(d=3, N=4, C=3, M=40),
     workloads.user_benchmark(d=4, N=4, C=3, M=200, seed=12),
     workloads.benchmark(d=9, N=3, C=2, M=120, seed=13),               # (9,9): not in the static set
