@@ -33,11 +33,14 @@ constexpr int kThreads = 256;
 #define SRMDP_LDG256 1    // 256-bit hot-line loads
 #endif
 #ifndef SRMDP_J_UNROLL
-#define SRMDP_J_UNROLL 2   // path-step loop unrolled by 2: X_{j+1} / X_{j+2} swap roles without register moves (+0.9%)
+#define SRMDP_J_UNROLL 2   // d <= 8: path-step loop unrolled by 2, X_{j+1} / X_{j+2} swap roles without register moves (+0.9% at d = 6; at d = 19 the doubled body costs 15% in instruction-cache misses, so 1 there)
 #endif
 constexpr int kJUnroll = SRMDP_J_UNROLL;
 #ifndef SRMDP_PREFETCH
-#define SRMDP_PREFETCH 0  // prefetch.global.L1 of the next hot line: measured -1.2% with the 256-bit loads
+#define SRMDP_PREFETCH 0  // prefetch of the next hot line, d <= 8 (0 none, 1 L1, 2 L2): measured -1.2% at d = 6 with the 256-bit loads
+#endif
+#ifndef SRMDP_PREFETCH_HD
+#define SRMDP_PREFETCH_HD 0   // d > 8: L1 prefetch measured -3% at d = 19 (4.34e9 vs 4.48e9), L2 -6%
 #endif
 
 // Row stride (doubles) of the shared-memory row tile [1 | x - r_k | S dW/dt]:
@@ -189,12 +192,16 @@ __device__ __forceinline__ void eval_block(const DevProblem& P, const double* __
   else zlin = zlin_exact<D, Q>(P, blk, a);
 }
 
-// L1 prefetch of a coefficient block (every 128-byte line it spans).
-template <int NHOT>
+// Prefetch of a coefficient block's hot part (every 128-byte line it spans)
+// into L1 (mode 1) or L2 (mode 2), issued before the next step's increments.
+template <int NHOT, int MODE>
 __device__ __forceinline__ void prefetch_block(const double* blk) {
-  if constexpr (SRMDP_PREFETCH != 0) {
+  if constexpr (MODE == 1) {
 #pragma unroll
     for (int off = 0; off < NHOT * 8; off += 128) asm volatile("prefetch.global.L1 [%0];" ::"l"((const char*)blk + off));
+  } else if constexpr (MODE == 2) {
+#pragma unroll
+    for (int off = 0; off < NHOT * 8; off += 128) asm volatile("prefetch.global.L2 [%0];" ::"l"((const char*)blk + off));
   }
 }
 
@@ -230,7 +237,8 @@ __device__ __forceinline__ void simulate_path(const DevProblem& P, const Grid& G
   }
   double acc = 0.0, zlin = 0.0, Y1 = 0.0, yv = 0.0;
   const int N = P.N;
-#pragma unroll kJUnroll
+  constexpr int JU = (D <= 8) ? kJUnroll : 1;
+#pragma unroll JU
   for (int j = i; j < N; ++j) {
     // Xn = X_{j+1}
     double zn = 0.0;
@@ -256,7 +264,7 @@ __device__ __forceinline__ void simulate_path(const DevProblem& P, const Grid& G
       asm volatile("ld.global.ca.u32 %0, [%1];" : "=r"(t2) : "l"(blk + 8));
       asm volatile("ld.global.ca.u32 %0, [%1];" : "=r"(t3) : "l"(blk + 12));
 #else
-      prefetch_block<2 * KC::N1 + 1>(blk);
+      prefetch_block<2 * KC::N1 + 1, (D > 8 ? SRMDP_PREFETCH_HD : SRMDP_PREFETCH)>(blk);
 #endif
       double Xnn[D];
       {
