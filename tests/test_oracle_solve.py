@@ -196,6 +196,34 @@ def test_cfg1_slope(orc):
     assert np.max(np.abs(t)) < 6.0
 
 
+def test_cfg1_exact_noise_model(orc):
+    """cfg1 (X = W, f = 0, g = 0.5 + 0.25 x): the Y response g(X_N) given x_i
+    is Gaussian with mean 0.5 + 0.25 x_i and variance 0.25^2 (N - i) dt, so the
+    per-cell OLS error is exactly N(0, sigma^2 (A^T A)^-1) given the design A
+    (SURVEY §8(c), cfg1 pin). chi^2 = e^T A^T A e / sigma^2 is chi^2_2 for every
+    (seed, i, cell): its mean (2) and its distribution pin the increment scale
+    sqrt(dt), the number of steps per path, the response assembly and the OLS."""
+    from scipy import stats
+    chis = []
+    for s in range(40):
+        w = workloads.cfg1(seed=500 + s)
+        P = orc.Problem(w)
+        tab, fb = P.solve()
+        assert fb == 0
+        N, dt = w["N"], w["T"] / w["N"]
+        for i in range(N):
+            sig2 = 0.25 ** 2 * (N - i) * dt
+            for k in range(P.K):
+                r = P.center(k)[0]
+                x = np.array([P.start_point(i, k, m)[0] for m in range(w["M"])])
+                A = np.stack([np.ones_like(x), x - r], axis=1)
+                e = tab[i, k, :2] - np.array([0.5 + 0.25 * r, 0.25])
+                chis.append(e @ (A.T @ A) @ e / sig2)
+    chis = np.array(chis)
+    assert abs(chis.mean() - 2.0) < 0.3, chis.mean()
+    assert stats.kstest(chis, stats.chi2(2).cdf).pvalue > 1e-3
+
+
 def test_truncation_binds(orc):
     w = dict(workloads.benchmark(d=2, N=3, C=3, M=64), C_y_override=0.3, C_z_override=0.05)
     P = orc.Problem(w)
