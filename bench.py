@@ -86,6 +86,25 @@ def fp64_peak():
     return 148 * 64 * 2 * 1.965e9 / 1e12, "derived: 148 SM x 64 FP64 FMA/clk x 2 x 1.965 GHz"
 
 
+def gather_block(w, path_steps_per_s):
+    """Secondary roofline: the per-lane coefficient gather through L1/L2. Bytes
+    per path-step = the hot part [beta^Y | W | S] read with 256-bit loads
+    (2(d+1)+1 doubles rounded up to 32 B); ceilings from tools/gather_bw.cu
+    (profiles/gather_bw.json: random lanes and warp-local lanes, same
+    occupancy). Context for the ALU roofline, not the headline."""
+    nhot = 2 * (w["d"] + 1) + 1
+    bps = ((nhot * 8 + 31) // 32) * 32
+    out = {"bytes_per_path_step": bps, "achieved_GBps": path_steps_per_s * bps / 1e9}
+    try:
+        g = json.load(open(os.path.join(ROOT, "profiles", "gather_bw.json")))
+        out["ceiling_random_lanes_GBps"] = g["random_ldg256"]["GB_per_s"]
+        out["ceiling_warp_local_GBps"] = g["local_ldg256"]["GB_per_s"]
+        out["source"] = "profiles/gather_bw.json (tools/gather_bw.cu)"
+    except Exception:
+        pass
+    return out
+
+
 def ncu_traffic():
     try:
         return json.load(open(os.path.join(ROOT, "profiles", "step_kernel_traffic.json")))
@@ -335,6 +354,7 @@ def main():
             "data": "synthetic (seeded Philox clouds of the §5.1 benchmark; no dataset)",
             "config": config_block(w, args),
             "roofline": roof,
+            "gather": gather_block(w, path_steps * args.steps / (total_ms / 1e3)),
             "cpu_baseline": cpu,
             "e2e": {"value": path_steps * args.steps / e2e_s, "unit": "path-steps/s",
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
