@@ -11,7 +11,7 @@ static cudaError_t prepare_impl(int C, size_t* smem, int* ctas) {
   *smem = SmemLayout<D, Q>::bytes(C);
   cudaError_t e = cudaFuncSetAttribute(step_kernel<D, Q, EQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)*smem);
   if (e != cudaSuccess) return e;
-  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(ctas, step_kernel<D, Q, EQ>, kThreads, *smem);
+  return fit_carveout((const void*)step_kernel<D, Q, EQ>, *smem, kThreads, ctas);
 }
 template <int D, int Q, bool EQ>
 static void step_impl(const DevProblem& P, int i, int64_t kb, int64_t nk, int grid, size_t smem, cudaStream_t s) {

@@ -6,6 +6,27 @@
 
 #include "problem.cuh"
 
+#include <cmath>
+
+// Smallest shared-memory carveout that still holds the resident CTAs: the
+// rest of the SM's 256 KB L1/shared array stays L1 for the gathered hot
+// lines (left to itself the driver picks 132 KB for 3 x 31 KB at d = 6).
+#ifndef SRMDP_CARVEOUT_FIT
+#define SRMDP_CARVEOUT_FIT 1
+#endif
+static inline cudaError_t fit_carveout(const void* f, size_t smem, int threads, int* ctas) {
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(ctas, f, threads, smem);
+  if (e != cudaSuccess || *ctas < 1 || !SRMDP_CARVEOUT_FIT) return e;
+  int dev = 0, maxsm = 0, reserved = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+  cudaDeviceGetAttribute(&reserved, cudaDevAttrReservedSharedMemoryPerBlock, dev);
+  if (maxsm <= 0) return cudaSuccess;
+  int pct = (int)std::ceil(100.0 * (double)(*ctas) * (double)(smem + reserved) / (double)maxsm);
+  pct = pct < 0 ? 0 : (pct > 100 ? 100 : pct);
+  return cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+}
+
 struct Ops {
   int D, Q;
   cudaError_t (*prepare)(int C, size_t* smem, int* ctas);     // equal-size grid

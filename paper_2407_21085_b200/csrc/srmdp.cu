@@ -483,7 +483,7 @@ static cudaError_t prepare_step(srmdp_t* h) {
   h->smem = step_smem_bytes(h->d, h->q, h->C);
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->smem);
   if (e != cudaSuccess) return e;
-  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(&h->ctas, k, kThreads, h->smem);
+  return fit_carveout(k, h->smem, kThreads, &h->ctas);
 }
 
 static void launch_step(srmdp_t* h, int i, int64_t kb, int64_t nk) {
