@@ -26,9 +26,6 @@ namespace srk {
 constexpr int kThreads = 256;
 
 // Kernel variants (A/B builds: build.py -DNAME=VALUE)
-#ifndef SRMDP_TOUCH
-#define SRMDP_TOUCH 0     // sector-touch loads instead of prefetch.global.L1 (measured slower)
-#endif
 #ifndef SRMDP_LDG256
 #define SRMDP_LDG256 1    // 256-bit hot-line loads
 #endif
@@ -254,27 +251,13 @@ __device__ __forceinline__ void simulate_path(const DevProblem& P, const Grid& G
       kn = k;
 #endif
       const double* blk = P.table + ((size_t)(j + 1) * (size_t)P.K_pad + kn) * (size_t)KC::NBP;
-#if SRMDP_TOUCH
-      // pull the block's 32-byte sectors into L1 with one 4-byte load each;
-      // the dummy registers stay live (empty asm below) so the warp never
-      // waits on them -- the loads complete under the increments / Euler work
-      uint32_t t0, t1, t2, t3;
-      asm volatile("ld.global.ca.u32 %0, [%1];" : "=r"(t0) : "l"(blk));
-      asm volatile("ld.global.ca.u32 %0, [%1];" : "=r"(t1) : "l"(blk + 4));
-      asm volatile("ld.global.ca.u32 %0, [%1];" : "=r"(t2) : "l"(blk + 8));
-      asm volatile("ld.global.ca.u32 %0, [%1];" : "=r"(t3) : "l"(blk + 12));
-#else
       prefetch_block<2 * KC::N1 + 1, (D > 8 ? SRMDP_PREFETCH_HD : SRMDP_PREFETCH)>(blk);
-#endif
       double Xnn[D];
       {
         double dW[Q];
         brownian<Q>(P, G, i, j + 1, k, m, dW);   // increments of step j+1
         euler<D, Q>(P, (double)(j + 1) * P.dt, Xn, dW, Xnn);
       }
-#if SRMDP_TOUCH
-      asm volatile("" ::"r"(t0), "r"(t1), "r"(t2), "r"(t3));
-#endif
       double a[D + 1];
       a[0] = 1.0;
 #pragma unroll
