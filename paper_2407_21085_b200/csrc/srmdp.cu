@@ -652,8 +652,8 @@ extern "C" srmdp_status srmdp_create(const srmdp_config* cfg, srmdp_t** out) {
   h->tabs = tabs;
 
   // launch configuration: persistent CTAs; the pass-2 records go to a per-CTA
-  // global scratch (L2-resident) so shared memory stays small and the L1 keeps
-  // room for the prefetched coefficient blocks (3 CTAs/SM at d <= 8)
+  // global scratch so shared memory stays small and the L1 keeps room for the
+  // gathered coefficient lines (3 CTAs/SM at d <= 8, 2 above)
   e = prepare_step(h);
   if (e != cudaSuccess || h->ctas < 1) {
     if (e == cudaSuccess) h->err = "step kernel does not fit on an SM";

@@ -8,13 +8,15 @@
 //          the path lands in, truncated evaluation (eq. TL) and
 //          the multistep response S_{Y,i+1} (eq. PsiM). The design
 //          row (1, x_i - r_k) and the Z responses S_{Y,i+1} dW_i / dt go to a
-//          shared-memory row buffer; owner-compute threads fold them into the
-//          Gram matrix and Z right-hand sides in a fixed order.
+//          shared-memory row tile, folded into the Gram matrix and Z
+//          right-hand sides in a fixed order (FP64 MMA for d >= 4, owner-
+//          compute threads below); (B, Y1, x_i - r_k) go to a per-CTA scratch.
 //  solve   Cholesky of the (d+1)^2 Gram (thread 0), q triangular solves
 //          -> beta^Z (same OLS minimiser as the paper's QR).
 //  pass 2  S_{Y,i} = S_{Y,i+1} + f_i(x_i, y_{i+1}(x_{i+1}), z_i(x_i)) dt with
-//          the fresh z_i of this cell, warp-shuffle + fixed-order
-//          block reduction of the Y right-hand side, solve -> beta^Y.
+//          the fresh z_i of this cell from the scratch records,
+//          warp-shuffle + fixed-order block reduction of the Y right-hand
+//          side, solve -> beta^Y.
 //  store   [beta^Y | beta^Z_1..q] into table[i][k] (docs/layout.md).
 // Reduction orders depend only on (M, thread count), never on the number of
 // ranks, so tables are bit-identical for every world size.
@@ -99,8 +101,8 @@ struct SmemLayout {
   // The solve-phase arrays (Gram/L, R_Z, beta, R_Y, warp partials, flag) alias
   // the row tile behind the reduction scratch `red`: they are only live after
   // the last round of pass 1 and die before the next cell's pass 1. Keeps a
-  // d = 6 CTA at 31 KB, so 3 CTAs/SM fit the 100 KB shared-memory carveout and
-  // L1 keeps ~130 KB for the coefficient hot lines.
+  // d = 6 CTA at 31 KB, so 3 CTAs/SM fit a 100 KB shared-memory carveout and
+  // L1 keeps the rest for the coefficient hot lines (fit_carveout, ops.h).
   using KC = KCfg<D, Q>;
   static constexpr int RED = (((KC::USE_MMA ? KC::ITEMS * 64 : KC::PAIRS) > kThreads
                                    ? (KC::USE_MMA ? KC::ITEMS * 64 : KC::PAIRS)
