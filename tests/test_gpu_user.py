@@ -50,6 +50,12 @@ SOLVE_CASES = [
          dyn_params=[0.05] * 10 + [0.0] * 100 + [0.2, 0.0, 0.1] * 10, f_params=[-0.03, 0.01, 0.1, -0.2, 0.05],
          g_params=[1.0] + [0.5] * 10),
     dict(workloads.benchmark(d=11, N=2, C=2, M=64, seed=15), grid="equiprobable"),   # EQ above d = 8
+    # maximum dimensions (d, q <= 32): one cell, affine dynamics
+    dict(workloads.cfg2(N=2, C=1, M=80), name="affine_d32q1", d=32, q=1, dyn="affine", C=1,
+         dyn_params=[0.05] * 32 + [0.0] * (32 * 32) + [0.3] * 32, f_params=[-0.03, 0.01, 0.2],
+         g_params=[1.0] + [0.1] * 32),
+    dict(workloads.cfg2(N=3, C=3, M=64), name="affine_d1q32", d=1, q=32, dyn="affine", C=3,
+         dyn_params=[0.05, 0.1] + [0.02] * 32, f_params=[-0.03, 0.01] + [0.01] * 32, g_params=[1.0, 0.5]),
 ]
 
 
