@@ -970,6 +970,8 @@ struct SrmdHeader {
 extern "C" srmdp_status srmdp_table_save(const srmdp_t* h, const char* path) {
   if (!h || !path) return SRMDP_E_ARG;
   if (h->valid_from >= h->N) { h->err = "table_save: no slice present"; return SRMDP_E_STATE; }
+  CK(h, cudaSetDevice(h->cfg.device), "cudaSetDevice");
+  CK(h, cudaStreamSynchronize(h->stream), "table_save: pending work");   // e.g. after srmdp_solve_async
   FILE* f = fopen(path, "wb");
   if (!f) { h->err = std::string("table_save: cannot open ") + path; return SRMDP_E_ARG; }
   SrmdHeader hd{{'S', 'R', 'M', 'D'}, 1, h->d, h->q, h->N, h->B_pad, hot_len(h->d), h->valid_from, h->K, h->cfg.seed};
@@ -1003,6 +1005,7 @@ extern "C" srmdp_status srmdp_table_load(srmdp_t* h, const char* path) {
     return SRMDP_E_ARG;
   }
   CK(h, cudaSetDevice(h->cfg.device), "cudaSetDevice");
+  CK(h, cudaStreamSynchronize(h->stream), "table_load: pending work");
   std::vector<double> buf((size_t)h->K * h->B_pad);
   for (int i = hd.i_lo; i < h->N; ++i) {
     if (fread(buf.data(), sizeof(double), buf.size(), f) != buf.size()) {
