@@ -68,22 +68,25 @@ def algorithmic_flops(w):
 
 
 def fp64_peak():
-    """Roofline denominator: MEASURED_PEAKS.json if it has FP64, else our
-    measured DFMA microbenchmark (profiles/), else the derivation from unit
-    counts and the max clock (148 SM x 64 FP64 lanes x 2 x 1.965 GHz)."""
+    """Roofline denominator of the ALU-bound step kernel: MEASURED_PEAKS.json
+    if it ever carries an FP64 entry, else the peak derived from unit counts and
+    the max clock (148 SM x 64 FP64 FMA/clk x 2 flop x 1.965 GHz
+    = 37.2 TFLOP/s). Returns (peak, source, measured DFMA microbenchmark or None)."""
+    measured = None
+    try:
+        m = json.load(open(os.path.join(ROOT, "profiles", "fp64_peak.json")))
+        measured = float(m["fp64_tflops_sustained"])
+    except Exception:
+        pass
     try:
         mp = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
         for k in ("fp64_tflops_sustained", "fp64_tflops"):
             if k in mp:
-                return float(mp[k]), "MEASURED_PEAKS.json:" + k
+                return float(mp[k]), "MEASURED_PEAKS.json:" + k, measured
     except Exception:
         pass
-    try:
-        m = json.load(open(os.path.join(ROOT, "profiles", "fp64_peak.json")))
-        return float(m["fp64_tflops_sustained"]), "measured DFMA microbenchmark (profiles/fp64_peak.json, sustained)"
-    except Exception:
-        pass
-    return 148 * 64 * 2 * 1.965e9 / 1e12, "derived: 148 SM x 64 FP64 FMA/clk x 2 x 1.965 GHz"
+    return (148 * 64 * 2 * 1.965e9 / 1e12, "derived (DESIGN.md §5): 148 SM x 64 FP64 FMA/clk x 2 x 1.965 GHz",
+            measured)
 
 
 def gather_block(w, path_steps_per_s):
@@ -304,14 +307,19 @@ def main():
     value = path_steps * args.steps / (total_ms / 1e3)
 
     # dominant kernel roofline: the fused step kernel (N launches per solve)
-    peak, peak_src = fp64_peak()
+    peak, peak_src, peak_meas = fp64_peak()
     flops = algorithmic_flops(w) / world         # per rank per solve
     launches_per_solve = st["kernel_launches"]
     achieved = flops * args.steps / (kern_ms / 1e3) / 1e12
     traffic = ncu_traffic()
     roof = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
-            "traffic": (traffic or {}).get("dram_bytes_per_launch"), "kernel": "srk::step_kernel<%d,%d>" % (w["d"], w["q"]),
-            "peak_source": peak_src, "flops_per_path_step": flops_per_path_step(w),
+            # ncu DRAM bytes per launch of this workload's captured launch (profiles/), else null
+            "traffic": (traffic or {}).get("dram_bytes_per_launch")
+            if (traffic or {}).get("launch", "").startswith(w["name"] + ",") else None,
+            "kernel": "srk::step_kernel<%d,%d>" % (w["d"], w["q"]),
+            "peak_source": peak_src,
+            "peak_measured_dfma": peak_meas, "frac_of_measured_dfma": (achieved / peak_meas) if peak_meas else None,
+            "flops_per_path_step": flops_per_path_step(w),
             "flops_per_path_start": flops_per_path_start(w),
             "kernel_share_of_step": kern_ms / total_ms, "avg_launch_ms": kern_ms / (args.steps * max(1, launches_per_solve))}
     solver.close()
