@@ -41,6 +41,7 @@ SOLVE_CASES = [
     dict(workloads.user_nonlinear(d=2, q=2, N=4, C=4, M=200, seed=10), C_z_override=0.3, C_y_override=0.6),
     workloads.user_cfg2(N=5, C=6, M=128),
     workloads.user_nonlinear(d=5, q=5, N=4, C=3, M=300, seed=16),    # MMA Gram path (d >= 4) with a user driver
+    dict(workloads.user_nonlinear(d=4, q=4, N=3, C=3, M=200, seed=18), C_z_override=0.2, C_y_override=0.55),
     workloads.user_nonlinear(d=6, q=2, N=3, C=2, M=257, seed=17),
     workloads.user_time(d=3, N=4, C=3, M=40),
     workloads.user_benchmark(d=4, N=4, C=3, M=200, seed=12),
