@@ -80,3 +80,40 @@ def test_product_does_not_import_oracle():
             if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
                 src = open(os.path.join(dirpath, f)).read()
                 assert "import oracle" not in src and "srmdp_oracle" not in src and "or_solve" not in src, f
+
+
+def test_create_validation_needs_no_gpu(lib):
+    """srmdp_create validates the configuration before touching CUDA, so every
+    rejection is testable on the CPU: status codes and messages (srmdp.h)."""
+    import workloads
+    base = workloads.benchmark(d=2, N=3, C=3, M=10)
+    cases = [
+        (dict(base, d=0, q=0), -1, "d and q"),
+        (dict(base, N=0), -1, "N must"),
+        (dict(base, T=0.0), -1, "T must"),
+        (dict(base, C=0), -1, "cells_per_dim"),
+        (dict(base, L=-1.0), -1, "L must"),
+        (dict(base, mu=0.0), -1, "mu must"),
+        (dict(base, M=2), -2, "M < d+1"),
+        (dict(base, C=3000), -7, "cells_per_dim > 2048"),
+        (dict(base, N=1 << 24), -7, "N >= 2^24"),
+        (dict(base, d=33, q=33, C=1, M=40), -7, "d, q <= 32"),
+        (dict(base, d=8, q=8, C=16, M=20), -7, "K = C^d"),
+        (dict(base, dyn="gbm", dyn_params=[0.1, 0.1, 0.2, 0.2], q=3), -1, "q == d"),
+        (dict(base, dyn="affine", dyn_params=[0.0]), -1, "parameter count"),
+        (dict(base, dyn="user"), -1, "user_src"),
+    ]
+    for w, status, msg in cases:
+        with pytest.raises(lib.SrmdpError) as e:
+            lib.Solver(w)
+        assert e.value.status == status, (w, e.value)
+        assert msg in str(e.value), (msg, str(e.value))
+    with pytest.raises(lib.SrmdpError) as e:           # world > 1 needs the NCCL id
+        lib.Solver(base, world=2, rank=0)
+    assert e.value.status == -1 and "nccl_unique_id" in str(e.value)
+    with pytest.raises(lib.SrmdpError) as e:
+        lib.Solver(base, world=2, rank=2, nccl_id=b"x" * 128)
+    assert e.value.status == -1
+    with pytest.raises(lib.SrmdpError) as e:           # P2P exchange excludes loopback
+        lib.Solver(base, world=2, flags=lib.FLAG_LOOPBACK | lib.FLAG_P2P_EXCHANGE)
+    assert e.value.status == -1
