@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define SRMDP_ABI_VERSION 1
+#define SRMDP_ABI_VERSION 2   /* 2: srmdp_config gained user_src / user_params / n_user_params */
 
 typedef struct srmdp srmdp_t; /* opaque: device table, streams, graph, NCCL comm */
 
