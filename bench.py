@@ -234,6 +234,9 @@ def main():
                     help="per-step slice exchange for N > 1: in-place ncclAllGather (default) or the fused "
                          "NVLink store epilogue (SRMDP_FLAG_P2P_EXCHANGE)")
     ap.add_argument("--ref-path-steps", type=float, default=2.0e8)
+    ap.add_argument("--e2e-mode", default="auto", choices=["auto", "create", "reseed"],
+                    help="e2e step: a fresh handle (create) or srmdp_reseed on one handle (reseed); "
+                         "auto = create at N = 1, reseed at N > 1")
     args = ap.parse_args()
 
     rank = int(os.environ.get("RANK", "0"))
@@ -328,26 +331,41 @@ def main():
     # create (uploads parameters) -> solve -> coeffs of every slice to pinned host memory -> destroy
     host = torch.empty((w["N"], st["K"], st["B"]), dtype=torch.float64).pin_memory()
     hnp = host.numpy()
+    # N = 1: every step is a fresh handle (create uploads the problem, destroy
+    # frees). N > 1: one handle (its NCCL communicator is set up once, as a
+    # serving process would), every step a new seed -- srmdp_reseed -- then
+    # solve and the coefficient download.
     e2e_times = []
+    persistent = None
+    reseed_mode = args.e2e_mode == "reseed" or (args.e2e_mode == "auto" and world > 1)
+    if reseed_mode:
+        persistent = srmdp.Solver(w, rank=rank, world=world, device=local, stream=stream.cuda_stream,
+                                  flags=xflag, nccl_id=fresh_nccl_id())
     for s in range(1 + args.steps):
         barrier()
         t0 = time.perf_counter()
-        sv = srmdp.Solver(w, rank=rank, world=world, device=local, stream=stream.cuda_stream,
-                          flags=xflag, nccl_id=fresh_nccl_id())
+        if persistent is None:
+            sv = srmdp.Solver(w, rank=rank, world=world, device=local, stream=stream.cuda_stream,
+                              flags=xflag, nccl_id=None)
+        else:
+            sv = persistent.reseed(args.seed + 1000 + s)
         sv.solve()
         for i in range(w["N"]):
             sv.coeffs(i, 1, hnp[i])
-        sv.close()
+        if persistent is None:
+            sv.close()
         barrier()
         if s > 0:
             e2e_times.append(time.perf_counter() - t0)
+    if persistent is not None:
+        persistent.close()
     e2e_s = float(sum(e2e_times))
     if world > 1:
         t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t[0])
     n_par = len(w.get("dyn_params", [])) + len(w.get("f_params", [])) + len(w.get("g_params", []))
-    h2d = 8 * (n_par + 3 * w["C"] + 2)
+    h2d = 8 * (n_par + 3 * w["C"] + 2) if not reseed_mode else 8     # problem upload, or the new seed
     d2h = 8 * w["N"] * st["K"] * st["B"]
 
     cpu = None
@@ -366,7 +384,8 @@ def main():
             "cpu_baseline": cpu,
             "e2e": {"value": path_steps * args.steps / e2e_s, "unit": "path-steps/s",
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                    "calls": "srmdp_create+srmdp_solve+srmdp_coeffs(all i, pinned host)+srmdp_destroy"},
+                    "calls": "srmdp_create+srmdp_solve+srmdp_coeffs(all i, pinned host)+srmdp_destroy"
+                    if not reseed_mode else "srmdp_reseed+srmdp_solve+srmdp_coeffs(all i, pinned host) on one handle per rank"},
             # step kernels + (fused exchange) the epoch / entry-barrier kernels and a signal + wait per slice
             "gpu_launches": (launches_per_solve + ((3 + 2 * w["N"]) if args.exchange == "p2p" else 0)) * args.steps,
             "clocks": clk.summary(),
