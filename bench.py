@@ -108,9 +108,26 @@ def gather_block(w, path_steps_per_s):
     return out
 
 
-def ncu_traffic():
+def ncu_traffic(name="cfg4"):
+    """ncu DRAM / L2 bytes of one captured step-kernel launch of workload
+    `name` (profiles/step_kernel_traffic*.json, from `ncu --set full`)."""
+    fn = "step_kernel_traffic.json" if name == "cfg4" else "step_kernel_traffic_%s.json" % name
     try:
-        return json.load(open(os.path.join(ROOT, "profiles", "step_kernel_traffic.json")))
+        t = json.load(open(os.path.join(ROOT, "profiles", fn)))
+        return t if t.get("launch", "").startswith(name + ",") else None
+    except Exception:
+        return None
+
+
+def executed_flops(name):
+    """FP64 flops the step kernels EXECUTE per solve, counted by ncu over every
+    launch of one solve (profiles/executed_flops.json: DFMA x 2 + DMUL + DADD
+    thread instructions + DMMA m8n8k4 x 512 per warp instruction), next to the
+    method's algorithmic count -- the certified contraction evaluates fewer
+    flops than the model credits."""
+    try:
+        e = json.load(open(os.path.join(ROOT, "profiles", "executed_flops.json")))
+        return e.get(name)
     except Exception:
         return None
 
@@ -210,6 +227,68 @@ def run_reference(args, w, rank):
     return 0
 
 
+def run_secondary(w, args, rank, world, local, dev, stream, fresh_nccl_id, barrier, flush, xflag, steps):
+    """BASELINE configs[4] (cfg5: §5.1 benchmark d = q = 19, N = 5, 2^19 cells,
+    M = 3200 -- the paper's largest row), measured in the same
+    run with the same timing rules: 1 warm-up, `steps` timed solves with L2
+    flushed, CUDA events on the library's stream, clocks sampled, max over
+    ranks. Its roofline: FP64 (credited and executed flops) and HBM (ncu DRAM
+    bytes of a captured launch; the 1.68 GB slices exceed L2)."""
+    import torch
+    import torch.distributed as dist
+    from paper_2407_21085_b200 import srmdp
+    solver = srmdp.Solver(w, rank=rank, world=world, device=local, stream=stream.cuda_stream,
+                          flags=srmdp.FLAG_TIME_KERNELS | xflag, nccl_id=fresh_nccl_id())
+    solver.solve()
+    barrier()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    kms = []
+    with ClockSampler(local) as clk:
+        barrier()
+        for s in range(steps):
+            flush.fill_(float(s))
+            ev[s][0].record(stream)
+            solver.solve_async()
+            ev[s][1].record(stream)
+            solver.wait()
+            kms.append(solver.stats()["kernel_ms"])
+        barrier()
+    tot = float(sum(a.elapsed_time(b) for a, b in ev))
+    kern = float(sum(kms))
+    if world > 1:
+        t = torch.tensor([tot, kern], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        tot, kern = float(t[0]), float(t[1])
+    st = solver.stats()
+    solver.close()
+    value = st["path_steps"] * steps / (tot / 1e3)
+    peak, _, peak_meas = fp64_peak()
+    achieved = algorithmic_flops(w) / world * steps / (kern / 1e3) / 1e12
+    ex = executed_flops(w["name"])
+    ex_tf = (ex["flop_per_solve"] / world * steps / (kern / 1e3) / 1e12) if ex else None
+    tr = ncu_traffic(w["name"])
+    hbm = None
+    if tr:
+        gbps = tr["dram_bytes_per_launch"] / (tr["duration_ms_ncu"] / 1e3) / 1e9
+        hbm_peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] \
+            if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6545.6
+        hbm = {"dram_GBps_ncu_launch": gbps, "peak_GBps": hbm_peak, "frac": gbps / hbm_peak,
+               "lts_GBps_ncu_launch": tr.get("lts_bytes_per_launch", 0) / (tr["duration_ms_ncu"] / 1e3) / 1e9
+               if tr.get("lts_bytes_per_launch") else None,
+               "launch": tr["launch"], "source": tr.get("source")}
+    return {"workload": w["name"], "d": w["d"], "q": w["q"], "N": w["N"], "K": w["C"] ** w["d"], "M": w["M"],
+            "path_steps_per_solve": st["path_steps"], "value": value, "unit": "path-steps/s", "steps": steps,
+            "warmup": 1, "ms_per_step": tot / steps, "kernel_share_of_step": kern / tot,
+            "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+                         "frac_of_measured_dfma": (achieved / peak_meas) if peak_meas else None,
+                         "executed_tflops": ex_tf, "executed_frac": (ex_tf / peak) if ex_tf else None,
+                         "flops_per_path_step": flops_per_path_step(w), "flops_per_path_start": flops_per_path_start(w)},
+            "hbm": hbm, "gather": gather_block(w, value), "clocks": clk.summary(),
+            "lp0_fallbacks": st["lp0_fallbacks"],
+            "launch": {"grid": st["grid"], "block": st["block"], "smem_bytes": st["smem_bytes"],
+                       "ctas_per_sm": st["ctas_per_sm"]}}
+
+
 def config_block(w, args):
     return {"workload": w["name"], "d": w["d"], "q": w["q"], "N": w["N"], "cells_per_dim": w["C"],
             "K": w["C"] ** w["d"], "M": w["M"], "problem": "PAPER.md §5.1 benchmark (X=W, mu=1, T=1, L=6.5)"
@@ -234,6 +313,8 @@ def main():
                     help="per-step slice exchange for N > 1: in-place ncclAllGather (default) or the fused "
                          "NVLink store epilogue (SRMDP_FLAG_P2P_EXCHANGE)")
     ap.add_argument("--ref-path-steps", type=float, default=2.0e8)
+    ap.add_argument("--no-cfg5", action="store_true", help="skip the secondary cfg5 (d = 19) block")
+    ap.add_argument("--cfg5-steps", type=int, default=2)
     ap.add_argument("--e2e-mode", default="auto", choices=["auto", "create", "reseed"],
                     help="e2e step: a fresh handle (create) or srmdp_reseed on one handle (reseed); "
                          "auto = create at N = 1, reseed at N > 1")
@@ -254,6 +335,9 @@ def main():
     from paper_2407_21085_b200 import srmdp
 
     torch.cuda.set_device(local)
+    if world > 1 and "NCCL_DEBUG" not in os.environ:
+        # NCCL's init log (ranks, NVLink / NVLS transport) on stderr, readable next to the JSON line
+        os.environ.update(NCCL_DEBUG="INFO", NCCL_DEBUG_SUBSYS="INIT", NCCL_DEBUG_FILE="/dev/stderr")
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
@@ -314,18 +398,27 @@ def main():
     flops = algorithmic_flops(w) / world         # per rank per solve
     launches_per_solve = st["kernel_launches"]
     achieved = flops * args.steps / (kern_ms / 1e3) / 1e12
-    traffic = ncu_traffic()
+    traffic = ncu_traffic(w["name"])
+    ex = executed_flops(w["name"])
+    ex_tf = (ex["flop_per_solve"] / world * args.steps / (kern_ms / 1e3) / 1e12) if ex else None
     roof = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
             # ncu DRAM bytes per launch of this workload's captured launch (profiles/), else null
-            "traffic": (traffic or {}).get("dram_bytes_per_launch")
-            if (traffic or {}).get("launch", "").startswith(w["name"] + ",") else None,
+            "traffic": (traffic or {}).get("dram_bytes_per_launch"),
+            "executed_tflops": ex_tf, "executed_frac": (ex_tf / peak) if ex_tf else None,
+            "executed_source": ex.get("source") if ex else None,
             "kernel": "srk::step_kernel<%d,%d>" % (w["d"], w["q"]),
             "peak_source": peak_src,
             "peak_measured_dfma": peak_meas, "frac_of_measured_dfma": (achieved / peak_meas) if peak_meas else None,
             "flops_per_path_step": flops_per_path_step(w),
             "flops_per_path_start": flops_per_path_start(w),
             "kernel_share_of_step": kern_ms / total_ms, "avg_launch_ms": kern_ms / (args.steps * max(1, launches_per_solve))}
+    gather_ms = float(st["gather_ms"]) / args.steps if world > 1 or args.exchange == "p2p" else 0.0
     solver.close()
+
+    secondary = None
+    if args.config == "cfg4" and not args.no_cfg5:
+        secondary = run_secondary(workloads.cfg5(seed=args.seed), args, rank, world, local, dev, stream,
+                                  fresh_nccl_id, barrier, flush, xflag, steps=args.cfg5_steps)
 
     # e2e: the user's call sequence through the C ABI with host buffers:
     # create (uploads parameters) -> solve -> coeffs of every slice to pinned host memory -> destroy
@@ -390,6 +483,8 @@ def main():
             "gpu_launches": (launches_per_solve + ((3 + 2 * w["N"]) if args.exchange == "p2p" else 0)) * args.steps,
             "clocks": clk.summary(),
             "lp0_fallbacks": st["lp0_fallbacks"],
+            "exchange_ms_per_solve": gather_ms,
+            "cfg5": secondary,
             "launch": {"grid": st["grid"], "block": st["block"], "smem_bytes": st["smem_bytes"],
                        "ctas_per_sm": st["ctas_per_sm"]},
         }

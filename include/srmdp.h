@@ -34,7 +34,8 @@
 extern "C" {
 #endif
 
-#define SRMDP_ABI_VERSION 2   /* 2: srmdp_config gained user_src / user_params / n_user_params */
+#define SRMDP_ABI_VERSION 3   /* 2: srmdp_config gained user_src / user_params / n_user_params;
+                                 3: srmdp_stats_t gained exact_z_evals / exact_z_i / gather_ms */
 
 typedef struct srmdp srmdp_t; /* opaque: device table, streams, graph, NCCL comm */
 
@@ -115,6 +116,11 @@ typedef struct {
                                      acquire flags at system scope order the stores against the next
                                      step's reads. NCCL is still used once, at create, to exchange
                                      the IPC handles (world > 1). */
+#define SRMDP_FLAG_P2P_SELF_PEER 64 /* test mode of P2P_EXCHANGE at world == 1: the kernels read and store
+                                     a second table on this GPU and the epilogue's peer-store loop
+                                     (n_peers = 1) writes every block into the handle's own table, the
+                                     one srmdp_coeffs reads: that table then holds exactly what the
+                                     peer stores delivered (no table_load in this mode) */
 
 typedef struct {
   int d, q, N;          /* state dim, Brownian dim, time steps */
@@ -179,12 +185,18 @@ srmdp_status srmdp_eval(const srmdp_t* h, int i, size_t n, const double* x, doub
  *  srmdp_solve_steps runs steps i_hi down to i_lo (inclusive) with direct
  *    launches; i_hi must be N-1 or one below the lowest slice already present
  *    (solved or loaded). Collective.
- *  srmdp_table_save writes the present slices to a file: magic "SRMD", then
- *    int32 {version=1, d, q, N, B_pad, hot_len, i_lo}, int64 K, uint64 seed,
- *    then (N - i_lo) x K x B_pad little-endian doubles, slices i_lo .. N-1 in
- *    the device block layout of docs/layout.md (rank-local; call on one rank).
- *  srmdp_table_load reads such a file into a handle created with the same
- *    (d, q, N, cells, seed, basis, grid); collective (every rank loads). */
+ *  srmdp_table_save writes the present slices to a file (the library's own
+ *    checkpoint format, SURVEY §5 "checkpoint / resume"): a 128-byte header --
+ *    magic "SRMD", int32 {version = 2, d, q, N, B_pad, hot_len, i_lo, lp0, grid,
+ *    dyn kind, f kind, g kind, cells_per_dim}, int64 {K, M}, uint64 seed,
+ *    double {T, L, mu, C_y, C_z}, uint64 FNV-1a hash of the parameter arrays
+ *    and the user source -- then (N - i_lo) x K x B_pad little-endian doubles,
+ *    slices i_lo .. N-1 in the device block layout of docs/layout.md
+ *    (rank-local; call on one rank).
+ *  srmdp_table_load reads such a file into a handle whose header matches in
+ *    every field but i_lo (the same problem, clouds and basis: anything else is
+ *    SRMDP_E_ARG); collective (every rank loads). Copies go through a pinned
+ *    buffer on the handle's stream. */
 srmdp_status srmdp_solve_steps(srmdp_t* h, int i_hi, int i_lo);
 srmdp_status srmdp_table_save(const srmdp_t* h, const char* path);
 srmdp_status srmdp_table_load(srmdp_t* h, const char* path);
@@ -192,6 +204,10 @@ srmdp_status srmdp_table_load(srmdp_t* h, const char* path);
 /* Per-step kernel durations of the last solve in ms, out[i] for step i
  * (needs SRMDP_FLAG_TIME_KERNELS; steps not run in the last call are 0). */
 srmdp_status srmdp_step_ms(const srmdp_t* h, double* out, int n);
+/* Per-step exchange durations (the ncclAllGather of slice i, or the fused
+ * exchange's flag wait) of the last solve in ms, out[i] for step i; same
+ * conditions as srmdp_step_ms, 0 where no exchange ran. */
+srmdp_status srmdp_exchange_ms(const srmdp_t* h, double* out, int n);
 
 /* Replace the Philox key (docs/streams.md §2) for the next srmdp_solve: a new,
  * independent set of clouds on the same problem (independent runs, e.g. the
@@ -219,6 +235,13 @@ typedef struct {
   int64_t K, K_pad, chunk, k_begin, k_end; /* sharding (docs/layout.md) */
   int B, B_pad;
   int grid, block, smem_bytes, ctas_per_sm; /* launch configuration of the step kernel */
+  /* ABI 3: */
+  uint64_t exact_z_evals;   /* path-step evaluations where the certificate (reading R23) could not rule
+                               out truncation and z was truncated per component (eq. TL) */
+  uint64_t exact_z_i;       /* the same for z_i(x_i) in the Y response (pass 2) */
+  double gather_ms;         /* sum of the per-step exchange durations (ncclAllGather or the fused
+                               flag wait) of the last solve, device-timed (needs SRMDP_FLAG_TIME_KERNELS;
+                               0 for world == 1 without FORCE_NCCL / P2P_EXCHANGE) */
 } srmdp_stats_t;
 
 srmdp_status srmdp_stats(const srmdp_t* h, srmdp_stats_t* out);

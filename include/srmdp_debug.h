@@ -22,8 +22,19 @@ extern "C" {
 srmdp_status srmdp_debug_trace(const srmdp_t* h, int i, int64_t k, int64_t m0, int64_t n,
                                double* x, int64_t* cell, double* dW);
 
+/* Re-run step i of the sweep with the cell-dump variant of the step kernel
+ * (same code as the product kernel plus stores; compiled for the static
+ * d = q in {1, 2, 4, 6, 11, 19}, equal-size grid): for the first dump_m paths
+ * of every cell of this rank's range, cell[kl][m][s] = located cell of
+ * X_{i+1+s} (s = 0 .. N-i-2) and x[kl][m][s][d] = X_{i+1+s} (s = 0 .. N-i-1),
+ * kl = k - k_begin. Needs slices i+1 .. N-1 present; rewrites slice i with the
+ * same values a solve gives. SRMDP_E_UNSUPPORTED for other (d, q) / NVRTC
+ * builds / the equal-probability grid. */
+srmdp_status srmdp_debug_step_dump(srmdp_t* h, int i, int dump_m, uint32_t* cell, double* x);
+
 /* Elementwise device detmath (docs/detmath.md): op 0 = dm_log(in) -> out0;
- * op 1 = dm_sincospi2(in) -> (out0 = sin, out1 = cos). */
+ * op 1 = dm_sincospi2(in) -> (out0 = sin, out1 = cos); op 2 = the path's
+ * correctly rounded sqrt (dsqrt_inrange, valid for 2^-970 <= in < 2^1023) -> out0. */
 srmdp_status srmdp_debug_detmath(int op, size_t n, const double* in, double* out0, double* out1);
 
 /* Philox4x32-10 on the device: ctr[n][4], key[2] -> out[n][4]. */

@@ -15,6 +15,8 @@ __global__ void detmath_kernel(const int op, const int64_t n, const double* __re
   T.stride = 1;
   if (op == 0) {
     o0[t] = dm_log(in[t], T);
+  } else if (op == 2) {
+    o0[t] = dsqrt_inrange(in[t]);   // Box-Muller's sqrt (in-range inputs only)
   } else {
     double s, c;
     dm_sincospi2(in[t], T, s, c);

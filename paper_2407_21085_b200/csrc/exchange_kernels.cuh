@@ -35,16 +35,31 @@ __global__ void exchange_signal_kernel(const FlagPtrs F, int world, int rank, in
 }
 
 // Before anything reads slice `slot` (or, for the entry slot, before the
-// first peer store): wait until every rank has published this epoch.
-__global__ void exchange_wait_kernel(const unsigned* own, int world, int slot, const unsigned* epoch) {
+// first peer store): wait until every rank has published this epoch. The spin
+// is bounded (timeout_ns of %globaltimer): a rank that never signals (died,
+// failed collective) sets err = 1 + slot instead of hanging this stream; the
+// host turns it into SRMDP_E_NCCL at srmdp_wait and the table is invalid.
+__device__ __forceinline__ uint64_t global_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+__global__ void exchange_wait_kernel(const unsigned* own, int world, int slot, const unsigned* epoch, unsigned* err,
+                                     uint64_t timeout_ns) {
   const int r = threadIdx.x;
   if (r >= world) return;
   const unsigned e = *epoch;
   const unsigned* p = own + (size_t)slot * world + r;
+  const uint64_t t0 = global_ns();
   unsigned v;
   for (;;) {
     asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     if ((int)(v - e) >= 0) break;
+    if (*(volatile unsigned*)err || global_ns() - t0 > timeout_ns) {   // give up (once one wait failed, all do)
+      atomicCAS(err, 0u, 1u + (unsigned)slot);
+      break;
+    }
     __nanosleep(200);
   }
   __threadfence_system();

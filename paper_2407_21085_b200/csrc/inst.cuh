@@ -18,6 +18,14 @@ static void step_impl(const DevProblem& P, int i, int64_t kb, int64_t nk, int gr
   step_kernel<D, Q, EQ><<<grid, kThreads, smem, s>>>(P, i, kb, nk);
 }
 template <int D, int Q>
+static void step_dump_impl(const DevProblem& P, int i, int64_t kb, int64_t nk, int grid, size_t smem, cudaStream_t s) {
+  // same shared-memory size and residency as step_kernel<D, Q, false>
+  if (cudaFuncSetAttribute(step_kernel<D, Q, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+      cudaSuccess)
+    return;   // the launch below then fails and cudaGetLastError reports it
+  step_kernel<D, Q, false, true><<<grid, kThreads, smem, s>>>(P, i, kb, nk);
+}
+template <int D, int Q>
 static void eval_impl(const DevProblem& P, int i, int64_t n, const double* x, double* y, double* z, cudaStream_t s) {
   const int bs = 128;
   eval_kernel<D, Q><<<(unsigned)((n + bs - 1) / bs), bs, 0, s>>>(P, i, n, x, y, z);
@@ -31,10 +39,15 @@ static void trace_impl(const DevProblem& P, int i, uint32_t k, int64_t m0, int64
 
 template <int D, int Q>
 Ops make_ops() {
+  // the cell-dump debug variant is compiled for the benchmark dimensions the
+  // parity suite checks (d = 1, 2, 4, 6, 11, 19)
+  constexpr bool dump = (D == Q) && (D == 1 || D == 2 || D == 4 || D == 6 || D == 11 || D == 19);
+  void (*sd)(const DevProblem&, int, int64_t, int64_t, int, size_t, cudaStream_t) = nullptr;
+  if constexpr (dump) sd = step_dump_impl<D, Q>;
   if constexpr (D <= 8)
     return Ops{D, Q, prepare_impl<D, Q, false>, step_impl<D, Q, false>, prepare_impl<D, Q, true>, step_impl<D, Q, true>,
-               eval_impl<D, Q>, trace_impl<D, Q>};
+               eval_impl<D, Q>, trace_impl<D, Q>, sd};
   else
     return Ops{D, Q, prepare_impl<D, Q, false>, step_impl<D, Q, false>, nullptr, nullptr, eval_impl<D, Q>,
-               trace_impl<D, Q>};
+               trace_impl<D, Q>, sd};
 }

@@ -35,6 +35,8 @@ struct Ops {
   void (*step_eq)(const srk::DevProblem&, int, int64_t, int64_t, int, size_t, cudaStream_t);   // (nullptr: d > 8)
   void (*eval)(const srk::DevProblem&, int, int64_t, const double*, double*, double*, cudaStream_t);
   void (*trace)(const srk::DevProblem&, int, uint32_t, int64_t, int64_t, double*, int64_t*, double*, cudaStream_t);
+  // debug variant of `step` that dumps located cells / states (srmdp_debug_step_dump); equal-size grid
+  void (*step_dump)(const srk::DevProblem&, int, int64_t, int64_t, int, size_t, cudaStream_t);
 };
 
 template <int D, int Q>

@@ -10,6 +10,7 @@
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>   // header-only NVTX v3: ranges cost nothing without a tool attached
 
 #include <chrono>
 #include <cmath>
@@ -46,6 +47,8 @@ struct NcclApi {
   ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
   ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*CommAbort)(ncclComm_t) = nullptr;
+  ncclResult_t (*CommGetAsyncError)(ncclComm_t, ncclResult_t*) = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
   std::string err;
 };
@@ -68,8 +71,11 @@ static NcclApi& nccl() {
   api.CommInitRank = (decltype(api.CommInitRank))dlsym(h, "ncclCommInitRank");
   api.AllGather = (decltype(api.AllGather))dlsym(h, "ncclAllGather");
   api.CommDestroy = (decltype(api.CommDestroy))dlsym(h, "ncclCommDestroy");
+  api.CommAbort = (decltype(api.CommAbort))dlsym(h, "ncclCommAbort");
+  api.CommGetAsyncError = (decltype(api.CommGetAsyncError))dlsym(h, "ncclCommGetAsyncError");
   api.GetErrorString = (decltype(api.GetErrorString))dlsym(h, "ncclGetErrorString");
-  api.ok = api.GetUniqueId && api.CommInitRank && api.AllGather && api.CommDestroy && api.GetErrorString;
+  api.ok = api.GetUniqueId && api.CommInitRank && api.AllGather && api.CommDestroy && api.GetErrorString &&
+           api.CommAbort && api.CommGetAsyncError;
   if (!api.ok) api.err = "libnccl.so.2 lacks a required symbol";
   return api;
 }
@@ -268,10 +274,11 @@ struct srmdp {
   cudaStream_t stream = nullptr;
   bool own_stream = false;
   double* d_table = nullptr;
+  double* d_replica = nullptr;       // P2P_SELF_PEER test mode: the table the kernels read
   double* d_params = nullptr;
   double* d_tabs = nullptr;
   double* d_scratch = nullptr;
-  unsigned long long* d_lp0 = nullptr;
+  unsigned long long* d_counters = nullptr;   // [lp0 fallbacks, exact z evals, exact z_i]
   double* d_io = nullptr;
   size_t io_cap = 0;
   DevProblem dp{};
@@ -289,6 +296,8 @@ struct srmdp {
   size_t ipc_bytes = 0;
   unsigned* d_flags = nullptr;       // own flags [N+1][world]
   unsigned* d_epoch = nullptr;
+  unsigned* d_xerr = nullptr;        // 1 + slot of a timed-out flag wait, else 0
+  uint64_t xchg_timeout_ns = 0;
   FlagPtrs fptr{};
   std::vector<void*> opened;         // peers' bases opened through IPC
   int launches_per_solve = 0;
@@ -296,9 +305,10 @@ struct srmdp {
   int graph_launches = 0;
   bool pending = false;
   std::chrono::steady_clock::time_point t_submit;
+  nvtxRangeId_t nvtx_solve = 0;
   int last_hi = 0, last_lo = 0;
-  std::vector<double> step_ms;
-  std::vector<cudaEvent_t> ev;
+  std::vector<double> step_ms, xchg_ms;
+  std::vector<cudaEvent_t> ev;       // [2N] step kernels, then [2N] exchanges
   srmdp_stats_t st{};
   mutable std::string err = "no error";
 };
@@ -377,6 +387,19 @@ static void dfree(const srmdp_t* h, void* p) {
     if (_e != cudaSuccess) return cuda_fail((h), _e, what); \
   } while (0)
 
+// A failed collective leaves the communicator unusable (peers may be blocked
+// in the same collective): abort it so no rank hangs, drop the table.
+static srmdp_status nccl_fail(srmdp_t* h, const char* what, ncclResult_t r) {
+  h->err = std::string(what) + ": " + nccl().GetErrorString(r) + " (communicator aborted; recreate the handle)";
+  if (h->comm) {
+    nccl().CommAbort(h->comm);
+    h->comm = nullptr;
+  }
+  h->valid_from = h->N;
+  h->solved = false;
+  return SRMDP_E_NCCL;
+}
+
 extern "C" srmdp_status srmdp_shard_plan(int64_t K, int world, int rank, int64_t out[4]) {
   if (K < 1 || world < 1 || rank < 0 || rank >= world || !out) return SRMDP_E_ARG;
   const int64_t chunk = (K + world - 1) / world;
@@ -428,6 +451,8 @@ static srmdp_status validate(const srmdp_config* c, std::string& err) {
   if (loopback && (c->flags & SRMDP_FLAG_FORCE_NCCL)) return bad(SRMDP_E_ARG, "LOOPBACK and FORCE_NCCL exclude each other");
   if ((c->flags & SRMDP_FLAG_P2P_EXCHANGE) && (loopback || c->world > kMaxRanks))
     return bad(SRMDP_E_ARG, "P2P_EXCHANGE needs world <= 8 and excludes LOOPBACK");
+  if ((c->flags & SRMDP_FLAG_P2P_SELF_PEER) && (!(c->flags & SRMDP_FLAG_P2P_EXCHANGE) || c->world != 1))
+    return bad(SRMDP_E_ARG, "P2P_SELF_PEER is a world == 1 test mode of P2P_EXCHANGE");
   if (c->dyn.kind < 0 || c->dyn.kind > 4 || c->driver.kind < 0 || c->driver.kind > 3 || c->terminal.kind < 0 ||
       c->terminal.kind > 2)
     return bad(SRMDP_E_ARG, "unknown problem family kind");
@@ -498,7 +523,7 @@ static void launch_step(srmdp_t* h, int i, int64_t kb, int64_t nk) {
 
 static srmdp_status enqueue_sweep(srmdp_t* h, int i_hi, int i_lo) {
   const bool timed = h->cfg.flags & SRMDP_FLAG_TIME_KERNELS;
-  CK(h, cudaMemsetAsync(h->d_lp0, 0, sizeof(unsigned long long), h->stream), "memset");
+  CK(h, cudaMemsetAsync(h->d_counters, 0, 3 * sizeof(unsigned long long), h->stream), "memset");
   const int64_t nk = h->k_end - h->k_begin;
   const bool loopback = h->cfg.flags & SRMDP_FLAG_LOOPBACK;
   h->launches_per_solve = 0;
@@ -507,10 +532,15 @@ static srmdp_status enqueue_sweep(srmdp_t* h, int i_hi, int i_lo) {
     // that peer has entered this sweep (slot N)
     epoch_kernel<<<1, 1, 0, h->stream>>>(h->d_epoch);
     exchange_signal_kernel<<<1, kMaxRanks, 0, h->stream>>>(h->fptr, h->cfg.world, h->cfg.rank, h->N, h->d_epoch);
-    exchange_wait_kernel<<<1, kMaxRanks, 0, h->stream>>>(h->d_flags, h->cfg.world, h->N, h->d_epoch);
+    exchange_wait_kernel<<<1, kMaxRanks, 0, h->stream>>>(h->d_flags, h->cfg.world, h->N, h->d_epoch, h->d_xerr,
+                                                         h->xchg_timeout_ns);
     CK(h, cudaGetLastError(), "exchange entry barrier");
   }
   for (int i = i_hi; i >= i_lo; --i) {
+    char rname[48];
+    snprintf(rname, sizeof(rname), "srmdp step i=%d", i);
+    nvtxRangePushA(rname);   // per time step (launch + exchange); inside graph capture it tags the nodes
+    struct Pop { ~Pop() { nvtxRangePop(); } } pop_at_scope_end;
     if (timed) CK(h, record_event(h, h->ev[2 * i]), "event");
     if (loopback) {
       for (int r = 0; r < h->cfg.world; ++r) {   // shards in sequence on one table
@@ -527,20 +557,21 @@ static srmdp_status enqueue_sweep(srmdp_t* h, int i_hi, int i_lo) {
     }
     CK(h, cudaGetLastError(), "step kernel launch");
     if (timed) CK(h, record_event(h, h->ev[2 * i + 1]), "event");
+    const bool xchg = h->p2p || h->comm;
+    if (timed && xchg) CK(h, record_event(h, h->ev[2 * h->N + 2 * i]), "event");
     if (h->p2p) {
       // blocks of slice i are in every table once all ranks have signalled
       exchange_signal_kernel<<<1, kMaxRanks, 0, h->stream>>>(h->fptr, h->cfg.world, h->cfg.rank, i, h->d_epoch);
-      exchange_wait_kernel<<<1, kMaxRanks, 0, h->stream>>>(h->d_flags, h->cfg.world, i, h->d_epoch);
+      exchange_wait_kernel<<<1, kMaxRanks, 0, h->stream>>>(h->d_flags, h->cfg.world, i, h->d_epoch, h->d_xerr,
+                                                           h->xchg_timeout_ns);
       CK(h, cudaGetLastError(), "exchange flags");
     } else if (h->comm) {
       double* slice = h->d_table + (size_t)i * h->K_pad * h->B_pad;
       const size_t cnt = (size_t)h->chunk * h->B_pad;
       ncclResult_t r = nccl().AllGather(slice + (size_t)h->cfg.rank * cnt, slice, cnt, ncclDouble, h->comm, h->stream);
-      if (r != ncclSuccess) {
-        h->err = std::string("ncclAllGather: ") + nccl().GetErrorString(r);
-        return SRMDP_E_NCCL;
-      }
+      if (r != ncclSuccess) return nccl_fail(h, "ncclAllGather", r);
     }
+    if (timed && xchg) CK(h, record_event(h, h->ev[2 * h->N + 2 * i + 1]), "event");
   }
   return SRMDP_OK;
 }
@@ -617,6 +648,11 @@ extern "C" srmdp_status srmdp_create(const srmdp_config* cfg, srmdp_t** out) {
   const size_t table_bytes = (size_t)h->N * h->K_pad * h->B_pad * sizeof(double);
   std::vector<double> tabs = grid_tables(h->C, cfg->L, cfg->mu, cfg->grid != 0);
   h->p2p = cfg->flags & SRMDP_FLAG_P2P_EXCHANGE;
+  {   // bounded flag waits of the fused exchange (exchange_wait_kernel)
+    const char* t = getenv("SRMDP_EXCHANGE_TIMEOUT_S");
+    const double sec = (t && atof(t) > 0) ? atof(t) : 60.0;
+    h->xchg_timeout_ns = (uint64_t)(sec * 1e9);
+  }
   const size_t flags_off = (table_bytes + 255) & ~(size_t)255;
   const size_t flags_bytes = (size_t)(h->N + 1) * cfg->world * sizeof(unsigned);
   if (h->p2p) {   // IPC-exportable allocation: [table | flags]
@@ -624,7 +660,9 @@ extern "C" srmdp_status srmdp_create(const srmdp_config* cfg, srmdp_t** out) {
     if ((e = ipc_alloc(cfg->device, &h->ipc_base, h->ipc_bytes)) != cudaSuccess ||
         (e = cudaMemsetAsync((char*)h->ipc_base + flags_off, 0, flags_bytes, h->stream)) != cudaSuccess ||
         (e = dalloc(h, &h->d_epoch, sizeof(unsigned))) != cudaSuccess ||
-        (e = cudaMemsetAsync(h->d_epoch, 0, sizeof(unsigned), h->stream)) != cudaSuccess) {
+        (e = cudaMemsetAsync(h->d_epoch, 0, sizeof(unsigned), h->stream)) != cudaSuccess ||
+        (e = dalloc(h, &h->d_xerr, sizeof(unsigned))) != cudaSuccess ||
+        (e = cudaMemsetAsync(h->d_xerr, 0, sizeof(unsigned), h->stream)) != cudaSuccess) {
       cuda_fail(h, e, "p2p table alloc");
       return fail(SRMDP_E_NOMEM);
     }
@@ -637,7 +675,7 @@ extern "C" srmdp_status srmdp_create(const srmdp_config* cfg, srmdp_t** out) {
   }
   if ((e = dalloc(h, &h->d_params, h->params.size() * sizeof(double))) != cudaSuccess ||
       (e = dalloc(h, &h->d_tabs, tabs.size() * sizeof(double))) != cudaSuccess ||
-      (e = dalloc(h, &h->d_lp0, sizeof(unsigned long long))) != cudaSuccess) {
+      (e = dalloc(h, &h->d_counters, 3 * sizeof(unsigned long long))) != cudaSuccess) {
     cuda_fail(h, e, "alloc");
     return fail(SRMDP_E_NOMEM);
   }
@@ -700,11 +738,24 @@ extern "C" srmdp_status srmdp_create(const srmdp_config* cfg, srmdp_t** out) {
   P.user_params = h->d_params + uoff;
   P.tabs = h->d_tabs;
   P.table = h->d_table;
+  if (cfg->flags & SRMDP_FLAG_P2P_SELF_PEER) {
+    // test mode of the fused exchange on one GPU: the kernels read and store
+    // into a replica, and the epilogue's peer-store loop (n_peers = 1) writes
+    // every block into the handle's own IPC table, which srmdp_coeffs reads --
+    // so that table holds only what the peer stores delivered
+    if ((e = dalloc(h, &h->d_replica, table_bytes)) != cudaSuccess) {
+      cuda_fail(h, e, "replica alloc");
+      return fail(SRMDP_E_NOMEM);
+    }
+    P.table = h->d_replica;
+    P.peer_table[0] = h->d_table;
+    P.n_peers = 1;
+  }
   P.by_scratch = h->d_scratch;
-  P.lp0_count = h->d_lp0;
+  P.counters = h->d_counters;
 
   if (cfg->flags & SRMDP_FLAG_TIME_KERNELS) {
-    h->ev.resize(2 * h->N);
+    h->ev.resize(4 * h->N);
     for (auto& x : h->ev) cudaEventCreate(&x);
   }
   if ((cfg->world > 1 && !(cfg->flags & SRMDP_FLAG_LOOPBACK)) || (cfg->flags & SRMDP_FLAG_FORCE_NCCL)) {
@@ -760,6 +811,7 @@ static srmdp_status finish_solve(srmdp_t* h, std::chrono::steady_clock::time_poi
 extern "C" srmdp_status srmdp_solve_async(srmdp_t* h) {
   if (!h) return SRMDP_E_ARG;
   h->t_submit = std::chrono::steady_clock::now();
+  h->nvtx_solve = nvtxRangeStartA("srmdp_solve");
   CK(h, cudaSetDevice(h->cfg.device), "cudaSetDevice");
   const bool use_graph = !(h->cfg.flags & SRMDP_FLAG_NO_GRAPH);
   if (use_graph) {
@@ -801,24 +853,51 @@ extern "C" srmdp_status srmdp_solve(srmdp_t* h) {
 }
 
 static srmdp_status finish_solve(srmdp_t* h, std::chrono::steady_clock::time_point t0) {
-  CK(h, cudaStreamSynchronize(h->stream), "solve");
-  unsigned long long lp0 = 0;
-  CK(h, cudaMemcpy(&lp0, h->d_lp0, sizeof(lp0), cudaMemcpyDeviceToHost), "lp0 count");
-  h->st.lp0_fallbacks = lp0;
+  cudaError_t se = cudaStreamSynchronize(h->stream);
+  if (h->comm) {   // errors a collective raised after it was enqueued (e.g. a peer failed)
+    ncclResult_t ae = ncclSuccess;
+    if (nccl().CommGetAsyncError(h->comm, &ae) != ncclSuccess || ae != ncclSuccess) return nccl_fail(h, "NCCL", ae);
+  }
+  if (se != cudaSuccess) return cuda_fail(h, se, "solve");
+  unsigned long long cnt[3] = {0, 0, 0};
+  CK(h, cudaMemcpy(cnt, h->d_counters, sizeof(cnt), cudaMemcpyDeviceToHost), "event counters");
+  if (h->p2p) {
+    unsigned xerr = 0;
+    CK(h, cudaMemcpy(&xerr, h->d_xerr, sizeof(xerr), cudaMemcpyDeviceToHost), "exchange status");
+    if (xerr) {
+      cudaMemset(h->d_xerr, 0, sizeof(unsigned));
+      h->valid_from = h->N;
+      h->solved = false;
+      h->err = "fused exchange: a peer rank did not publish slot " + std::to_string(xerr - 1) +
+               " within the timeout (SRMDP_EXCHANGE_TIMEOUT_S); the table is invalid";
+      return SRMDP_E_NCCL;
+    }
+  }
+  h->st.lp0_fallbacks = cnt[0];
+  h->st.exact_z_evals = cnt[1];
+  h->st.exact_z_i = cnt[2];
   h->st.kernel_launches = h->launches_per_solve;
   if (h->cfg.flags & SRMDP_FLAG_TIME_KERNELS) {
-    double tot = 0;
+    double tot = 0, xt = 0;
     h->step_ms.assign(h->N, 0.0);
+    h->xchg_ms.assign(h->N, 0.0);
     for (int i = h->last_lo; i <= h->last_hi; ++i) {
       float ms = 0;
       CK(h, cudaEventElapsedTime(&ms, h->ev[2 * i], h->ev[2 * i + 1]), "event time");
       h->step_ms[i] = ms;
       tot += ms;
+      if (h->p2p || h->comm) {
+        CK(h, cudaEventElapsedTime(&ms, h->ev[2 * h->N + 2 * i], h->ev[2 * h->N + 2 * i + 1]), "event time");
+        h->xchg_ms[i] = ms;
+        xt += ms;
+      }
     }
     h->st.kernel_ms = tot;
+    h->st.gather_ms = xt;
   }
   h->valid_from = h->last_lo;
   h->solved = (h->valid_from == 0);
+  if (h->nvtx_solve) { nvtxRangeEnd(h->nvtx_solve); h->nvtx_solve = 0; }
   h->st.solve_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
   return SRMDP_OK;
 }
@@ -960,64 +1039,115 @@ extern "C" srmdp_status srmdp_solve_steps(srmdp_t* h, int i_hi, int i_lo) {
   return finish_solve(h, t0);
 }
 
+// Checkpoint file (srmdp.h): header v2 identifies the problem completely --
+// every input of the sweep's arithmetic -- so a slice set can only be loaded
+// into a handle that would have computed the same slices.
 struct SrmdHeader {
   char magic[4];
   int32_t version, d, q, N, B_pad, hot, i_lo;
-  int64_t K;
+  int32_t lp0, grid, dyn, fk, gk, C;
+  int64_t K, M;
   uint64_t seed;
+  double T, L, mu, C_y, C_z;
+  uint64_t problem_hash;   // FNV-1a over the parameter arrays and the user source
 };
 
+static uint64_t fnv1a(uint64_t h, const void* p, size_t n) {
+  const unsigned char* b = (const unsigned char*)p;
+  for (size_t t = 0; t < n; ++t) { h ^= b[t]; h *= 0x100000001b3ull; }
+  return h;
+}
+
+static SrmdHeader make_header(const srmdp_t* h) {
+  SrmdHeader hd;
+  memset(&hd, 0, sizeof(hd));   // padding bytes too: the header is compared field by field, written as bytes
+  memcpy(hd.magic, "SRMD", 4);
+  hd.version = 2;
+  hd.d = h->d; hd.q = h->q; hd.N = h->N; hd.B_pad = h->B_pad; hd.hot = hot_len(h->d); hd.i_lo = h->valid_from;
+  hd.lp0 = h->cfg.lp0 ? 1 : 0; hd.grid = h->cfg.grid; hd.dyn = h->cfg.dyn.kind; hd.fk = h->cfg.driver.kind;
+  hd.gk = h->cfg.terminal.kind; hd.C = h->C;
+  hd.K = h->K; hd.M = h->M; hd.seed = h->cfg.seed;
+  hd.T = h->cfg.T; hd.L = h->cfg.L; hd.mu = h->cfg.mu; hd.C_y = h->C_y; hd.C_z = h->C_z;
+  uint64_t ph = 0xcbf29ce484222325ull;
+  ph = fnv1a(ph, h->params.data(), h->params.size() * sizeof(double));
+  ph = fnv1a(ph, h->user_src.data(), h->user_src.size());
+  hd.problem_hash = ph;
+  return hd;
+}
+
+// One slice at a time through a pinned staging buffer, on the handle's stream
+// (ordered with the solves that produce / consume the table).
 extern "C" srmdp_status srmdp_table_save(const srmdp_t* h, const char* path) {
   if (!h || !path) return SRMDP_E_ARG;
   if (h->valid_from >= h->N) { h->err = "table_save: no slice present"; return SRMDP_E_STATE; }
   CK(h, cudaSetDevice(h->cfg.device), "cudaSetDevice");
   CK(h, cudaStreamSynchronize(h->stream), "table_save: pending work");   // e.g. after srmdp_solve_async
+  const size_t n = (size_t)h->K * h->B_pad;
+  double* buf = nullptr;
+  CK(h, cudaMallocHost(&buf, n * sizeof(double)), "table_save: pinned buffer");
   FILE* f = fopen(path, "wb");
-  if (!f) { h->err = std::string("table_save: cannot open ") + path; return SRMDP_E_ARG; }
-  SrmdHeader hd{{'S', 'R', 'M', 'D'}, 1, h->d, h->q, h->N, h->B_pad, hot_len(h->d), h->valid_from, h->K, h->cfg.seed};
+  if (!f) { cudaFreeHost(buf); h->err = std::string("table_save: cannot open ") + path; return SRMDP_E_ARG; }
+  const SrmdHeader hd = make_header(h);
   bool ok = fwrite(&hd, sizeof(hd), 1, f) == 1;
-  std::vector<double> buf((size_t)h->K * h->B_pad);
+  cudaError_t e = cudaSuccess;
   for (int i = h->valid_from; ok && i < h->N; ++i) {
-    cudaError_t e = cudaMemcpy(buf.data(), h->d_table + (size_t)i * h->K_pad * h->B_pad, buf.size() * sizeof(double),
-                               cudaMemcpyDeviceToHost);
-    if (e != cudaSuccess) { fclose(f); return cuda_fail(h, e, "table_save copy"); }
-    ok = fwrite(buf.data(), sizeof(double), buf.size(), f) == buf.size();
+    e = cudaMemcpyAsync(buf, h->d_table + (size_t)i * h->K_pad * h->B_pad, n * sizeof(double), cudaMemcpyDeviceToHost,
+                        h->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
+    if (e != cudaSuccess) break;
+    ok = fwrite(buf, sizeof(double), n, f) == n;
   }
   ok = (fclose(f) == 0) && ok;
+  cudaFreeHost(buf);
+  if (e != cudaSuccess) return cuda_fail(h, e, "table_save copy");
   if (!ok) { h->err = "table_save: write failed"; return SRMDP_E_ARG; }
   return SRMDP_OK;
 }
 
 extern "C" srmdp_status srmdp_table_load(srmdp_t* h, const char* path) {
   if (!h || !path) return SRMDP_E_ARG;
+  if (h->d_replica) { h->err = "table_load: not in the P2P_SELF_PEER test mode"; return SRMDP_E_UNSUPPORTED; }
   FILE* f = fopen(path, "rb");
   if (!f) { h->err = std::string("table_load: cannot open ") + path; return SRMDP_E_ARG; }
   SrmdHeader hd;
-  if (fread(&hd, sizeof(hd), 1, f) != 1 || memcmp(hd.magic, "SRMD", 4) != 0 || hd.version != 1) {
+  if (fread(&hd, sizeof(hd), 1, f) != 1 || memcmp(hd.magic, "SRMD", 4) != 0 || hd.version != 2) {
     fclose(f);
-    h->err = "table_load: not an SRMD v1 file";
+    h->err = "table_load: not an SRMD v2 file";
     return SRMDP_E_ARG;
   }
-  if (hd.d != h->d || hd.q != h->q || hd.N != h->N || hd.K != h->K || hd.B_pad != h->B_pad ||
-      hd.hot != hot_len(h->d) || hd.seed != h->cfg.seed || hd.i_lo < 0 || hd.i_lo >= h->N) {
+  SrmdHeader mine = make_header(h);
+  mine.i_lo = hd.i_lo;
+  if (memcmp(&mine, &hd, sizeof(hd)) != 0 || hd.i_lo < 0 || hd.i_lo >= h->N) {
     fclose(f);
-    h->err = "table_load: file does not match this problem (d, q, N, K, layout, seed)";
+    h->err = "table_load: file does not match this problem (d, q, N, cells, M, T, L, mu, C_y, C_z, basis, grid, "
+             "families, parameters, user source, seed)";
     return SRMDP_E_ARG;
   }
   CK(h, cudaSetDevice(h->cfg.device), "cudaSetDevice");
   CK(h, cudaStreamSynchronize(h->stream), "table_load: pending work");
-  std::vector<double> buf((size_t)h->K * h->B_pad);
+  const size_t n = (size_t)h->K * h->B_pad;
+  double* buf = nullptr;
+  cudaError_t e = cudaMallocHost(&buf, n * sizeof(double));
+  if (e != cudaSuccess) { fclose(f); return cuda_fail(h, e, "table_load: pinned buffer"); }
+  srmdp_status st = SRMDP_OK;
   for (int i = hd.i_lo; i < h->N; ++i) {
-    if (fread(buf.data(), sizeof(double), buf.size(), f) != buf.size()) {
-      fclose(f);
+    if (fread(buf, sizeof(double), n, f) != n) {
       h->err = "table_load: truncated file";
-      return SRMDP_E_ARG;
+      st = SRMDP_E_ARG;
+      break;
     }
-    cudaError_t e = cudaMemcpy(h->d_table + (size_t)i * h->K_pad * h->B_pad, buf.data(), buf.size() * sizeof(double),
-                               cudaMemcpyHostToDevice);
-    if (e != cudaSuccess) { fclose(f); return cuda_fail(h, e, "table_load copy"); }
+    e = cudaMemcpyAsync(h->d_table + (size_t)i * h->K_pad * h->B_pad, buf, n * sizeof(double), cudaMemcpyHostToDevice,
+                        h->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);   // buf is reused for the next slice
+    if (e != cudaSuccess) { st = cuda_fail(h, e, "table_load copy"); break; }
   }
   fclose(f);
+  cudaFreeHost(buf);
+  if (st != SRMDP_OK) {   // the table may be partly overwritten: nothing is present any more
+    h->valid_from = h->N;
+    h->solved = false;
+    return st;
+  }
   h->valid_from = hd.i_lo;
   h->solved = (hd.i_lo == 0);
   return SRMDP_OK;
@@ -1026,6 +1156,12 @@ extern "C" srmdp_status srmdp_table_load(srmdp_t* h, const char* path) {
 extern "C" srmdp_status srmdp_step_ms(const srmdp_t* h, double* out, int n) {
   if (!h || !out || n != h->N) return SRMDP_E_ARG;
   for (int i = 0; i < n; ++i) out[i] = (i < (int)h->step_ms.size()) ? h->step_ms[i] : 0.0;
+  return SRMDP_OK;
+}
+
+extern "C" srmdp_status srmdp_exchange_ms(const srmdp_t* h, double* out, int n) {
+  if (!h || !out || n != h->N) return SRMDP_E_ARG;
+  for (int i = 0; i < n; ++i) out[i] = (i < (int)h->xchg_ms.size()) ? h->xchg_ms[i] : 0.0;
   return SRMDP_OK;
 }
 
@@ -1044,11 +1180,13 @@ extern "C" void srmdp_destroy(srmdp_t* h) {
   }
   if (h->stream) {
     dfree(h, h->d_epoch);
+    dfree(h, h->d_xerr);
+    dfree(h, h->d_replica);
     dfree(h, h->d_table);
     dfree(h, h->d_params);
     dfree(h, h->d_tabs);
     dfree(h, h->d_scratch);
-    dfree(h, h->d_lp0);
+    dfree(h, h->d_counters);
     dfree(h, h->d_io);
     cudaStreamSynchronize(h->stream);
   }
@@ -1140,8 +1278,37 @@ extern "C" srmdp_status srmdp_debug_trace(const srmdp_t* h, int i, int64_t k, in
   return SRMDP_OK;
 }
 
+extern "C" srmdp_status srmdp_debug_step_dump(srmdp_t* h, int i, int dump_m, uint32_t* cell, double* x) {
+  if (!h || i < 0 || i >= h->N || dump_m < 1 || dump_m > h->M || !cell || !x) return SRMDP_E_ARG;
+  if (h->jit || h->cfg.grid || !h->ops->step_dump || (h->cfg.flags & SRMDP_FLAG_LOOPBACK)) {
+    h->err = "step_dump: only the static equal-size kernels of d = q in {1, 2, 4, 6, 11, 19}";
+    return SRMDP_E_UNSUPPORTED;
+  }
+  if (h->valid_from > i + 1) { h->err = "step_dump: slices i+1 .. N-1 must be present"; return SRMDP_E_STATE; }
+  CK(h, cudaSetDevice(h->cfg.device), "cudaSetDevice");
+  const int64_t nk = h->k_end - h->k_begin;
+  const int steps = h->N - i;
+  const size_t nc = (size_t)nk * dump_m * (size_t)(steps > 1 ? steps - 1 : 0);
+  const size_t nx = (size_t)nk * dump_m * (size_t)steps * h->d;
+  srmdp_status s = ensure_io(h, (nx + nc / 2 + 2) * sizeof(double));
+  if (s != SRMDP_OK) return s;
+  DevProblem P = h->dp;
+  P.dump_m = dump_m;
+  P.dump_x = h->d_io;
+  P.dump_cell = reinterpret_cast<uint32_t*>(h->d_io + nx);
+  CK(h, cudaMemsetAsync(h->d_counters, 0, 3 * sizeof(unsigned long long), h->stream), "memset");
+  if (nk > 0) h->ops->step_dump(P, i, h->k_begin, nk, h->grid, h->smem, h->stream);
+  CK(h, cudaGetLastError(), "step dump kernel");
+  CK(h, cudaMemcpyAsync(x, P.dump_x, nx * sizeof(double), cudaMemcpyDeviceToHost, h->stream), "dump d2h");
+  if (nc) CK(h, cudaMemcpyAsync(cell, P.dump_cell, nc * sizeof(uint32_t), cudaMemcpyDeviceToHost, h->stream), "dump d2h");
+  CK(h, cudaStreamSynchronize(h->stream), "step dump");
+  if (h->valid_from == i + 1) h->valid_from = i;
+  h->solved = (h->valid_from == 0);
+  return SRMDP_OK;
+}
+
 extern "C" srmdp_status srmdp_debug_detmath(int op, size_t n, const double* in, double* out0, double* out1) {
-  if ((op != 0 && op != 1) || !in || !out0 || (op == 1 && !out1)) return SRMDP_E_ARG;
+  if (op < 0 || op > 2 || !in || !out0 || (op == 1 && !out1)) return SRMDP_E_ARG;
   if (n == 0) return SRMDP_OK;
   double* d = nullptr;
   cudaError_t e = cudaMalloc(&d, (3 * n + 512) * sizeof(double));

@@ -122,6 +122,13 @@ struct SmemLayout {
   __host__ __device__ static size_t bytes(int C) { return step_smem_bytes(D, Q, C); }
 };
 
+// Warp-aggregated event count (one atomic per warp and event site); only
+// executed where the event happens, so the certified fast paths pay nothing.
+__device__ __forceinline__ void count_event(unsigned long long* c) {
+  const unsigned mask = __activemask();
+  if ((int)(threadIdx.x & 31) == __ffs(mask) - 1) atomicAdd(c, (unsigned long long)__popc(mask));
+}
+
 // Exact evaluation of the q Z blocks: zlin = sum_l w_l T_{C_z}(beta^{Z_l} . a).
 template <int D, int Q>
 __device__ __forceinline__ double zlin_exact(const DevProblem& P, const double* __restrict__ blk, const double (&a)[D + 1]) {
@@ -187,8 +194,12 @@ __device__ __forceinline__ void eval_block(const DevProblem& P, const double* __
 #pragma unroll
   for (int p = 1; p <= D; ++p) hm = max(hm, __double2hiint(a[p]) & 0x7fffffff);
   const double amax = __hiloint2double(hm, 0xffffffff);
-  if (S * amax <= P.C_z_safe) zlin = wv;
-  else zlin = zlin_exact<D, Q>(P, blk, a);
+  if (S * amax <= P.C_z_safe) {
+    zlin = wv;
+  } else {
+    zlin = zlin_exact<D, Q>(P, blk, a);
+    count_event(P.counters + 1);
+  }
 }
 
 // Prefetch of a coefficient block's hot part (every 128-byte line it spans)
@@ -216,9 +227,10 @@ __device__ __forceinline__ void prefetch_block(const double* blk) {
 // latency, is what it costs: 256-bit instead of 128-bit loads gained 7%, an
 // explicit L1 prefetch now loses 1%. (Two paths per thread for ILP measured
 // slower: 2.43e10 vs 2.65e10.)
-template <int D, int Q, bool EQ>
+template <int D, int Q, bool EQ, bool DUMP>
 __device__ __forceinline__ void simulate_path(const DevProblem& P, const Grid& G, const int (&cc)[D], int i,
-                                              uint32_t k, uint32_t m, double* row, double& Bout, double& Y1out) {
+                                              uint32_t k, uint32_t m, double* row, double& Bout, double& Y1out,
+                                              int64_t kl) {
   using KC = KCfg<D, Q>;
   double Xn[D];
   start_point<D, EQ>(P, G, cc, i, k, m, Xn);
@@ -252,6 +264,14 @@ __device__ __forceinline__ void simulate_path(const DevProblem& P, const Grid& G
 #ifdef SRMDP_EXPERIMENT_GATHER_SELF   // timing experiment only (wrong results): every gather hits the start cell
       kn = k;
 #endif
+      if constexpr (DUMP) {   // debug build (srmdp_debug_step_dump): the cell and state this loop located
+        if ((int64_t)m < P.dump_m) {
+          const int64_t s = (kl * P.dump_m + m) * (int64_t)(N - i);
+          P.dump_cell[(kl * P.dump_m + m) * (int64_t)(N - i - 1) + (j - i)] = kn;
+#pragma unroll
+          for (int l = 0; l < D; ++l) P.dump_x[(s + (j - i)) * D + l] = Xn[l];
+        }
+      }
       const double* blk = P.table + ((size_t)(j + 1) * (size_t)P.K_pad + kn) * (size_t)KC::NBP;
       prefetch_block<2 * KC::N1 + 1, (D > 8 ? SRMDP_PREFETCH_HD : SRMDP_PREFETCH)>(blk);
       double Xnn[D];
@@ -269,6 +289,13 @@ __device__ __forceinline__ void simulate_path(const DevProblem& P, const Grid& G
       for (int l = 0; l < D; ++l) Xn[l] = Xnn[l];
     } else {
       yv = g_eval<D>(P, Xn);                     // y_N := g
+      if constexpr (DUMP) {
+        if ((int64_t)m < P.dump_m) {
+          const int64_t s = (kl * P.dump_m + m) * (int64_t)(N - i);
+#pragma unroll
+          for (int l = 0; l < D; ++l) P.dump_x[(s + (j - i)) * D + l] = Xn[l];
+        }
+      }
     }
     if (j == i) {
       Y1 = yv;
@@ -417,7 +444,10 @@ __device__ void chol_solve(const double* L, const double* r, double* b) {
 
 // EQ: equal-probability strata (binary-search locate) — a template parameter so
 // the equal-size grid's hot loop carries no grid branch (a runtime branch cost 4%).
-template <int D, int Q, bool EQ>
+// DUMP: debug variant (srmdp_debug_step_dump) that also writes the located
+// cells and states of the first dump_m paths of every cell; otherwise the
+// same code.
+template <int D, int Q, bool EQ, bool DUMP = false>
 __global__ void __launch_bounds__(kThreads, KCfg<D, Q>::CTAS)
 step_kernel(const DevProblem P, const int i, const int64_t k_begin, const int64_t nk) {
   using KC = KCfg<D, Q>;
@@ -502,7 +532,7 @@ step_kernel(const DevProblem P, const int i, const int64_t k_begin, const int64_
 #if SRMDP_USER_F
         simulate_path_user<D, Q, EQ>(P, G, cc, i, k, (uint32_t)m, row, Bv, Y1);
 #else
-        simulate_path<D, Q, EQ>(P, G, cc, i, k, (uint32_t)m, row, Bv, Y1);
+        simulate_path<D, Q, EQ, DUMP>(P, G, cc, i, k, (uint32_t)m, row, Bv, Y1, kl);
 #endif
         const double sc = Bv * P.inv_dt;
 #pragma unroll
@@ -694,6 +724,7 @@ step_kernel(const DevProblem P, const int i, const int64_t k_begin, const int64_
           for (int p = 0; p < KC::N1; ++p) v = fma(sBZ[l * KC::N1 + p], a[p], v);
           zl = fma(zweight(P, l), trunc_L(v, P.C_z), zl);
         }
+        count_event(P.counters + 2);
       }
       const double Sm = BYs[m] + f_eval(P, BYs[M + m], zl) * dt;
 #endif
@@ -720,7 +751,7 @@ step_kernel(const DevProblem P, const int i, const int64_t k_begin, const int64_
       } else {
         sBY[0] = sRY[0] / (double)M;               // eq. lp0:explicit
         for (int p = 1; p < KC::N1; ++p) sBY[p] = 0.0;
-        if (!P.lp0) atomicAdd(P.lp0_count, 1ull);  // rank-deficient LP1 fallback (R15)
+        if (!P.lp0) atomicAdd(P.counters, 1ull);   // rank-deficient LP1 fallback (R15)
       }
     }
     __syncthreads();

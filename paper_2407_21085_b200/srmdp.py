@@ -25,6 +25,7 @@ FLAG_FORCE_NCCL = 4
 FLAG_LOOPBACK = 8
 FLAG_JIT = 16
 FLAG_P2P_EXCHANGE = 32
+FLAG_P2P_SELF_PEER = 64
 
 STATUS = {0: "SRMDP_OK", -1: "SRMDP_E_ARG", -2: "SRMDP_E_PRECOND", -3: "SRMDP_E_STATE", -4: "SRMDP_E_CUDA",
           -5: "SRMDP_E_NCCL", -6: "SRMDP_E_NOMEM", -7: "SRMDP_E_UNSUPPORTED", -8: "SRMDP_E_JIT"}
@@ -66,6 +67,7 @@ class srmdp_stats_t(ctypes.Structure):
         ("K", ctypes.c_int64), ("K_pad", ctypes.c_int64), ("chunk", ctypes.c_int64),
         ("k_begin", ctypes.c_int64), ("k_end", ctypes.c_int64), ("B", ctypes.c_int), ("B_pad", ctypes.c_int),
         ("grid", ctypes.c_int), ("block", ctypes.c_int), ("smem_bytes", ctypes.c_int), ("ctas_per_sm", ctypes.c_int),
+        ("exact_z_evals", ctypes.c_uint64), ("exact_z_i", ctypes.c_uint64), ("gather_ms", ctypes.c_double),
     ]
 
 
@@ -89,6 +91,7 @@ SIGNATURES = {
     "srmdp_table_save": (ctypes.c_int, [_H, ctypes.c_char_p]),
     "srmdp_table_load": (ctypes.c_int, [_H, ctypes.c_char_p]),
     "srmdp_step_ms": (ctypes.c_int, [_H, _PD, ctypes.c_int]),
+    "srmdp_exchange_ms": (ctypes.c_int, [_H, _PD, ctypes.c_int]),
     "srmdp_last_error": (ctypes.c_char_p, [_H]),
     "srmdp_nccl_unique_id": (ctypes.c_int, [ctypes.c_void_p]),
     "srmdp_stats": (ctypes.c_int, [_H, ctypes.POINTER(srmdp_stats_t)]),
@@ -97,6 +100,7 @@ SIGNATURES = {
     "srmdp_jit_check": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                        ctypes.c_char_p, ctypes.c_char_p, ctypes.c_size_t]),
     "srmdp_debug_trace": (ctypes.c_int, [_H, ctypes.c_int, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, _PD, _P64, _PD]),
+    "srmdp_debug_step_dump": (ctypes.c_int, [_H, ctypes.c_int, ctypes.c_int, _PU32, _PD]),
     "srmdp_debug_detmath": (ctypes.c_int, [ctypes.c_int, ctypes.c_size_t, _PD, _PD, _PD]),
     "srmdp_debug_philox": (ctypes.c_int, [ctypes.c_size_t, _PU32, _PU32, _PU32]),
 }
@@ -268,6 +272,12 @@ def srmdp_step_ms(h, N: int) -> np.ndarray:
     return out
 
 
+def srmdp_exchange_ms(h, N: int) -> np.ndarray:
+    out = np.zeros(N)
+    _check(library().srmdp_exchange_ms(h, _dp(out), N), h)
+    return out
+
+
 def srmdp_destroy(h):
     if h:
         library().srmdp_destroy(h)
@@ -312,6 +322,9 @@ class Solver:
     def step_ms(self):
         return srmdp_step_ms(self.h, self.N)
 
+    def exchange_ms(self):
+        return srmdp_exchange_ms(self.h, self.N)
+
     def stats(self):
         return srmdp_stats(self.h)
 
@@ -331,6 +344,15 @@ class Solver:
         w = np.empty((n, steps, self.q))
         _check(library().srmdp_debug_trace(self.h, i, k, m0, n, _dp(x), c.ctypes.data_as(_P64), _dp(w)), self.h)
         return x, c, w
+
+    def step_dump(self, i, dump_m):
+        """srmdp_debug_step_dump: cells[kl][m][N-i-1], x[kl][m][N-i][d] as the step kernel located them."""
+        st = srmdp_stats(self.h)
+        nk, steps = st["k_end"] - st["k_begin"], self.N - i
+        c = np.zeros((nk, dump_m, steps - 1), dtype=np.uint32)
+        x = np.empty((nk, dump_m, steps, self.d))
+        _check(library().srmdp_debug_step_dump(self.h, i, dump_m, c.ctypes.data_as(_PU32), _dp(x)), self.h)
+        return c, x
 
     def close(self):
         srmdp_destroy(self.h)

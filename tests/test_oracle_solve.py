@@ -333,3 +333,17 @@ def test_benchmark_d2_vs_nested_monte_carlo(orc):
     m, se = e.mean(0), e.std(0, ddof=1) / math.sqrt(len(e))
     assert abs(m[0] - y_n) < 4 * math.hypot(se[0], se_yn) + 3e-3, (m[0], y_n)
     assert abs(m[1] - z_n.mean()) < 4 * math.hypot(se[1], se_zn) + 1e-2, (m[1], z_n)
+
+
+def test_rank_deficient_clouds_fall_back(orc):
+    """Reading R15 (rank d+1 only with probability 1): with L = 1e-10
+    the middle cell of each dimension is 6.7e-11 wide, so the QR |R_jj| of
+    that coordinate is ~1e-11 of the constant's and the (i,k) regression falls
+    back to LP0 -- in exactly the cells with a middle coordinate, at every
+    step. The GPU parity suite (test_gpu_parity SOLVE_CASES) compares these
+    fallback counts and coefficients with the kernel's Cholesky diag(L) test."""
+    for d, N, M, seed in ((2, 4, 200, 28), (4, 3, 120, 29), (11, 2, 24, 30)):
+        w = dict(workloads.benchmark(d=d, N=N, C=3, M=M, seed=seed), L=1e-10)
+        tab, fb = orc.Problem(w).solve()
+        assert fb == N * (3 ** d - 2 ** d), (d, fb)
+        assert np.all(np.isfinite(tab))

@@ -28,8 +28,11 @@ for r in rows:
         continue
     if r[0]:
         cur_line = "%s:%s" % (fname, r[0])
-    sass = r[3]
-    if not sass or not r[2] or r[2] == "...":
+    sass = r[3].strip()
+    # with --print-source=cuda,sass every CUDA source line also has an
+    # aggregate row ("-" in the SASS column) repeating the counts of the SASS
+    # rows below it: counting it too doubled every total (round-1 summaries)
+    if not sass or sass == "-" or not r[2] or r[2] == "...":
         continue
     op = sass.split()[0] if not sass.startswith("@") else sass.split()[1]
     op = op.split(".")[0]
