@@ -30,6 +30,7 @@ __global__ void eval_kernel(const DevProblem P, const int i, const int64_t n, co
     kn = kn * (uint32_t)P.C + (uint32_t)c;
     a[1 + l] = x[l] - __ldg(cen + c);
   }
+  SRK_CHECK(kn < (uint64_t)P.K && i < P.N, "eval cell");
   const double* blk = P.table + ((size_t)i * (size_t)P.K_pad + kn) * (size_t)KC::NBP;
   double v = 0.0;
 #pragma unroll

@@ -35,6 +35,10 @@ constexpr int kThreads = 256;
 #define SRMDP_J_UNROLL 2   // d <= 8: path-step loop unrolled by 2, X_{j+1} / X_{j+2} swap roles without register moves (+0.9% at d = 6; at d = 19 the doubled body costs 15% in instruction-cache misses, so 1 there)
 #endif
 constexpr int kJUnroll = SRMDP_J_UNROLL;
+#ifndef SRMDP_PASS2_UNROLL
+#define SRMDP_PASS2_UNROLL 1   // records of several paths in flight per thread (pass 2 is latency-bound on the scratch reads)
+#endif
+constexpr int kPass2Unroll = SRMDP_PASS2_UNROLL;
 #ifndef SRMDP_PREFETCH
 #define SRMDP_PREFETCH 0  // prefetch of the next hot line, d <= 8 (0 none, 1 L1, 2 L2): measured -1.2% at d = 6 with the 256-bit loads
 #endif
@@ -86,7 +90,19 @@ struct KCfg {
   static constexpr int QB = (NCOL + 7) / 8;         // 8-column blocks of C
   static constexpr int TILES = PB * QB - PB * (PB - 1) / 2;   // blocks with qb >= pb
   static constexpr int NW = kThreads / 32;
-  static constexpr int KSPLIT = (TILES >= NW) ? 1 : (NW / TILES >= 8 ? 8 : (NW / TILES >= 4 ? 4 : (NW / TILES >= 2 ? 2 : 1)));
+  // row slices per 8x8 tile: the smallest split that gives every warp the
+  // same number of (tile, slice) items (d = 8, 11: 5 tiles -> 40 items;
+  // d = 19: 12 tiles -> 24 items), so no warp idles at the barrier after the
+  // fold; the old rule split only when there were fewer tiles than warps
+#ifndef SRMDP_KSPLIT_BALANCE
+#define SRMDP_KSPLIT_BALANCE 1
+#endif
+  static constexpr int KSPLIT_OLD = (TILES >= NW) ? 1 : (NW / TILES >= 8 ? 8 : (NW / TILES >= 4 ? 4 : (NW / TILES >= 2 ? 2 : 1)));
+  static constexpr int KSPLIT_BAL = (TILES % NW == 0) ? 1 : ((2 * TILES) % NW == 0 ? 2 : ((4 * TILES) % NW == 0 ? 4 : 8));
+  // (the balanced split only where its partials fit the row tile beside the solve arrays, SmemLayout)
+  static constexpr int SOLVE_LEN = N1 * N1 + 2 * NZ + 2 * N1 + (kThreads / 32) * N1 + 2 + N1 + 2;
+  static constexpr bool BAL_FITS = TILES * KSPLIT_BAL * 64 + SOLVE_LEN + 2 <= ROWS * row_stride(D, Q);
+  static constexpr int KSPLIT = (SRMDP_KSPLIT_BALANCE && BAL_FITS) ? KSPLIT_BAL : KSPLIT_OLD;
   static constexpr int ITEMS = TILES * KSPLIT;      // (tile, row slice) work items
   static constexpr int NI = (ITEMS + NW - 1) / NW;  // items per warp
   // odd row stride (spreads banks); MMA fragment loads of the padding columns
@@ -107,8 +123,10 @@ struct SmemLayout {
   static constexpr int RED = (((KC::USE_MMA ? KC::ITEMS * 64 : KC::PAIRS) > kThreads
                                    ? (KC::USE_MMA ? KC::ITEMS * 64 : KC::PAIRS)
                                    : kThreads) + 1) & ~1;
-  static constexpr int SOLVE = KC::N1 * KC::N1 + 2 * KC::NZ + 2 * KC::N1 + (kThreads / 32) * KC::N1 + 2 + KC::N1 + 2;
+  static constexpr int SOLVE = KC::SOLVE_LEN;
   static_assert(RED + SOLVE <= KC::ROWS * KC::ROW, "solve arrays must fit in the row tile");
+  static_assert(!KC::USE_MMA || KC::ITEMS * 64 <= RED, "MMA tile partials must fit the reduction scratch");
+  static_assert(!KC::USE_MMA || 8 * (KC::QB - 1) + 7 < KC::ROW + 8, "MMA fragment columns stay within a row + padding");
   __host__ __device__ static int tabs(int C) { return smem_tabs_len(D, C); }
   __host__ __device__ static int rows(int C) { return tabs(C); }
   __host__ __device__ static int L(int C) { return rows(C) + RED; }
@@ -150,9 +168,15 @@ __device__ __forceinline__ double zlin_exact(const DevProblem& P, const double* 
 // Fast path (one 128-byte line for d <= 6): when S * max(1, max_p |a_p|) is
 // below C_z no component can be truncated, so zlin = W . a (same value up to
 // rounding order, reading R23); otherwise the exact per-component path.
+// Counting the exact evaluations (srmdp_stats.exact_z_evals): 1 = a
+// warp-aggregated atomic inside the exact branch, 2 = a per-thread register
+// count flushed once per path (the hot loop only increments it).
+#ifndef SRMDP_COUNT_EXACT
+#define SRMDP_COUNT_EXACT 1
+#endif
 template <int D, int Q>
 __device__ __forceinline__ void eval_block(const DevProblem& P, const double* __restrict__ blk,
-                                           const double (&a)[D + 1], double& y, double& zlin) {
+                                           const double (&a)[D + 1], double& y, double& zlin, int& nexact) {
   using KC = KCfg<D, Q>;
   constexpr int NHOT = 2 * KC::N1 + 1;
   double yv = 0.0, wv = 0.0, S = 0.0;
@@ -198,7 +222,11 @@ __device__ __forceinline__ void eval_block(const DevProblem& P, const double* __
     zlin = wv;
   } else {
     zlin = zlin_exact<D, Q>(P, blk, a);
+#if SRMDP_COUNT_EXACT == 1
     count_event(P.counters + 1);
+#elif SRMDP_COUNT_EXACT == 2
+    ++nexact;
+#endif
   }
 }
 
@@ -247,6 +275,7 @@ __device__ __forceinline__ void simulate_path(const DevProblem& P, const Grid& G
     for (int l = 0; l < D; ++l) Xn[l] = X1[l];
   }
   double acc = 0.0, zlin = 0.0, Y1 = 0.0, yv = 0.0;
+  int nexact = 0;
   const int N = P.N;
   constexpr int JU = (D <= 8) ? kJUnroll : 1;
 #pragma unroll JU
@@ -267,11 +296,13 @@ __device__ __forceinline__ void simulate_path(const DevProblem& P, const Grid& G
       if constexpr (DUMP) {   // debug build (srmdp_debug_step_dump): the cell and state this loop located
         if ((int64_t)m < P.dump_m) {
           const int64_t s = (kl * P.dump_m + m) * (int64_t)(N - i);
+          SRK_CHECK(j - i < N - i - 1, "dump index");
           P.dump_cell[(kl * P.dump_m + m) * (int64_t)(N - i - 1) + (j - i)] = kn;
 #pragma unroll
           for (int l = 0; l < D; ++l) P.dump_x[(s + (j - i)) * D + l] = Xn[l];
         }
       }
+      SRK_CHECK(kn < (uint64_t)P.K && j + 1 < P.N, "gathered cell / slice");
       const double* blk = P.table + ((size_t)(j + 1) * (size_t)P.K_pad + kn) * (size_t)KC::NBP;
       prefetch_block<2 * KC::N1 + 1, (D > 8 ? SRMDP_PREFETCH_HD : SRMDP_PREFETCH)>(blk);
       double Xnn[D];
@@ -284,7 +315,7 @@ __device__ __forceinline__ void simulate_path(const DevProblem& P, const Grid& G
       a[0] = 1.0;
 #pragma unroll
       for (int l = 0; l < D; ++l) a[1 + l] = Xn[l] - center_of<EQ>(P, G, c[l]);
-      eval_block<D, Q>(P, blk, a, yv, zn);       // y_{j+1}(x_{j+1}), z_{j+1}(x_{j+1})
+      eval_block<D, Q>(P, blk, a, yv, zn, nexact);   // y_{j+1}(x_{j+1}), z_{j+1}(x_{j+1})
 #pragma unroll
       for (int l = 0; l < D; ++l) Xn[l] = Xnn[l];
     } else {
@@ -307,6 +338,13 @@ __device__ __forceinline__ void simulate_path(const DevProblem& P, const Grid& G
   }
   Bout = yv + acc;                                 // g(x_N) + sum
   Y1out = Y1;
+#if SRMDP_COUNT_EXACT == 2
+  {   // one warp-aggregated atomic per path round
+    const unsigned mask = __activemask();
+    const unsigned tot = __reduce_add_sync(mask, (unsigned)nexact);
+    if (tot && (int)(threadIdx.x & 31) == __ffs(mask) - 1) atomicAdd(P.counters + 1, (unsigned long long)tot);
+  }
+#endif
 }
 
 #if SRMDP_USER_F
@@ -348,6 +386,7 @@ __device__ __forceinline__ void simulate_path_user(const DevProblem& P, const Gr
         kn = kn * (uint32_t)P.C + (uint32_t)c;
         a[1 + l] = Xn[l] - G.cen[c];
       }
+      SRK_CHECK(kn < (uint64_t)P.K && j + 1 < P.N, "gathered cell / slice (user driver)");
       const double* blk = P.table + ((size_t)(j + 1) * (size_t)P.K_pad + kn) * (size_t)KC::NBP;
       double v = 0.0;
 #pragma unroll
@@ -471,6 +510,16 @@ step_kernel(const DevProblem P, const int i, const int64_t k_begin, const int64_
   constexpr int SB = scratch_stride(D);
   double* BYs = P.by_scratch + (size_t)blockIdx.x * (size_t)P.M * SB;   // this CTA's pass-2 records
 
+#if SRMDP_BOUNDS_CHECK
+  {   // the carve-up (tables, row tile + MMA padding, solve arrays) fits the launch's dynamic shared memory
+    unsigned dyn;
+    asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(dyn));
+    SRK_CHECK((size_t)(SL::rows(C) + KC::ROWS * KC::ROW + 8) * 8 <= dyn, "row tile in shared memory");
+    SRK_CHECK((size_t)(SL::W(C) + KC::N1 + 1) * 8 <= dyn, "solve arrays in shared memory");
+    SRK_CHECK((size_t)(SL::rows(C) + SL::RED) <= (size_t)SL::L(C), "reduction scratch");
+    SRK_CHECK(k_begin >= 0 && k_begin + nk <= P.K, "cell range");
+  }
+#endif
   {   // grid tables, then the detmath tables replicated entry by entry (DetTabs)
     const int off = tabs_det_off(C);
     for (int t = tid; t < off; t += kThreads) sm[t] = P.tabs[t];
@@ -537,6 +586,7 @@ step_kernel(const DevProblem P, const int i, const int64_t k_begin, const int64_
         const double sc = Bv * P.inv_dt;
 #pragma unroll
         for (int l = 0; l < Q; ++l) row[1 + D + l] = row[1 + D + l] * sc;   // S_{Z,i} = S_{Y,i+1} dW_i / dt
+        SRK_CHECK(blockIdx.x < gridDim.x && m < M, "pass-2 record");
         BYs[m] = Bv;                               // scratch is field-major (coalesced)
         BYs[M + m] = Y1;
         if constexpr (store_design(D)) {
@@ -684,6 +734,7 @@ step_kernel(const DevProblem P, const int i, const int64_t k_begin, const int64_
     double ry[KC::N1];
 #pragma unroll
     for (int p = 0; p < KC::N1; ++p) ry[p] = 0.0;
+#pragma unroll kPass2Unroll
     for (int64_t m = tid; m < M; m += kThreads) {
       double a[KC::N1];
       a[0] = 1.0;
@@ -755,6 +806,7 @@ step_kernel(const DevProblem P, const int i, const int64_t k_begin, const int64_
       }
     }
     __syncthreads();
+    SRK_CHECK(i >= 0 && i < P.N && (int64_t)k < P.K, "epilogue block");
     double* dst = P.table + ((size_t)i * (size_t)P.K_pad + k) * (size_t)KC::NBP;
     for (int b = tid; b < KC::NBP; b += kThreads) {
       double v = 0.0;
