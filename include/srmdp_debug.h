@@ -24,7 +24,8 @@ srmdp_status srmdp_debug_trace(const srmdp_t* h, int i, int64_t k, int64_t m0, i
 
 /* Re-run step i of the sweep with the cell-dump variant of the step kernel
  * (same code as the product kernel plus stores; compiled for the static
- * d = q in {1, 2, 4, 6, 11, 19}, equal-size grid): for the first dump_m paths
+ * BM-dynamics (X = W) kernels of d = q in {1, 2, 4, 6, 11, 19}, equal-size
+ * grid -- the kernels the §5.1 benchmark runs): for the first dump_m paths
  * of every cell of this rank's range, cell[kl][m][s] = located cell of
  * X_{i+1+s} (s = 0 .. N-i-2) and x[kl][m][s][d] = X_{i+1+s} (s = 0 .. N-i-1),
  * kl = k - k_begin. Needs slices i+1 .. N-1 present; rewrites slice i with the

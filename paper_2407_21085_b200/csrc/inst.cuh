@@ -6,24 +6,25 @@
 
 using namespace srk;
 
-template <int D, int Q, bool EQ>
+template <int D, int Q, bool EQ, int DK = -1>
 static cudaError_t prepare_impl(int C, size_t* smem, int* ctas) {
   *smem = SmemLayout<D, Q>::bytes(C);
-  cudaError_t e = cudaFuncSetAttribute(step_kernel<D, Q, EQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)*smem);
+  cudaError_t e = cudaFuncSetAttribute(step_kernel<D, Q, EQ, false, DK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)*smem);
   if (e != cudaSuccess) return e;
-  return fit_carveout((const void*)step_kernel<D, Q, EQ>, *smem, kThreads, ctas);
+  return fit_carveout((const void*)step_kernel<D, Q, EQ, false, DK>, *smem, kThreads, ctas);
 }
-template <int D, int Q, bool EQ>
+template <int D, int Q, bool EQ, int DK = -1>
 static void step_impl(const DevProblem& P, int i, int64_t kb, int64_t nk, int grid, size_t smem, cudaStream_t s) {
-  step_kernel<D, Q, EQ><<<grid, kThreads, smem, s>>>(P, i, kb, nk);
+  step_kernel<D, Q, EQ, false, DK><<<grid, kThreads, smem, s>>>(P, i, kb, nk);
 }
 template <int D, int Q>
 static void step_dump_impl(const DevProblem& P, int i, int64_t kb, int64_t nk, int grid, size_t smem, cudaStream_t s) {
-  // same shared-memory size and residency as step_kernel<D, Q, false>
-  if (cudaFuncSetAttribute(step_kernel<D, Q, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
-      cudaSuccess)
+  // same code as step_kernel<D, Q, false, false, DYN_BM> plus the dump stores; same shared memory
+  if (cudaFuncSetAttribute(step_kernel<D, Q, false, true, DYN_BM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)smem) != cudaSuccess)
     return;   // the launch below then fails and cudaGetLastError reports it
-  step_kernel<D, Q, false, true><<<grid, kThreads, smem, s>>>(P, i, kb, nk);
+  step_kernel<D, Q, false, true, DYN_BM><<<grid, kThreads, smem, s>>>(P, i, kb, nk);
 }
 template <int D, int Q>
 static void eval_impl(const DevProblem& P, int i, int64_t n, const double* x, double* y, double* z, cudaStream_t s) {
@@ -44,10 +45,17 @@ Ops make_ops() {
   constexpr bool dump = (D == Q) && (D == 1 || D == 2 || D == 4 || D == 6 || D == 11 || D == 19);
   void (*sd)(const DevProblem&, int, int64_t, int64_t, int, size_t, cudaStream_t) = nullptr;
   if constexpr (dump) sd = step_dump_impl<D, Q>;
+  // BM-specialised kernel for the q = d benchmark dynamics (X = W)
+  cudaError_t (*pb)(int, size_t*, int*) = nullptr;
+  void (*sb)(const DevProblem&, int, int64_t, int64_t, int, size_t, cudaStream_t) = nullptr;
+  if constexpr (D == Q) {
+    pb = prepare_impl<D, Q, false, DYN_BM>;
+    sb = step_impl<D, Q, false, DYN_BM>;
+  }
   if constexpr (D <= 8)
     return Ops{D, Q, prepare_impl<D, Q, false>, step_impl<D, Q, false>, prepare_impl<D, Q, true>, step_impl<D, Q, true>,
-               eval_impl<D, Q>, trace_impl<D, Q>, sd};
+               eval_impl<D, Q>, trace_impl<D, Q>, sd, pb, sb};
   else
     return Ops{D, Q, prepare_impl<D, Q, false>, step_impl<D, Q, false>, nullptr, nullptr, eval_impl<D, Q>,
-               trace_impl<D, Q>, sd};
+               trace_impl<D, Q>, sd, pb, sb};
 }

@@ -35,8 +35,11 @@ struct Ops {
   void (*step_eq)(const srk::DevProblem&, int, int64_t, int64_t, int, size_t, cudaStream_t);   // (nullptr: d > 8)
   void (*eval)(const srk::DevProblem&, int, int64_t, const double*, double*, double*, cudaStream_t);
   void (*trace)(const srk::DevProblem&, int, uint32_t, int64_t, int64_t, double*, int64_t*, double*, cudaStream_t);
-  // debug variant of `step` that dumps located cells / states (srmdp_debug_step_dump); equal-size grid
+  // debug variant of `step_bm` that dumps located cells / states (srmdp_debug_step_dump)
   void (*step_dump)(const srk::DevProblem&, int, int64_t, int64_t, int, size_t, cudaStream_t);
+  // the equal-size-grid kernel with the dynamics fixed to BM (X = W, the §5.1 benchmark)
+  cudaError_t (*prepare_bm)(int C, size_t* smem, int* ctas);
+  void (*step_bm)(const srk::DevProblem&, int, int64_t, int64_t, int, size_t, cudaStream_t);
 };
 
 template <int D, int Q>

@@ -502,7 +502,14 @@ static cudaError_t record_event(srmdp_t* h, cudaEvent_t e) {
 
 // Step-kernel attributes and residency: the static instantiation or the NVRTC
 // build (sized with the same step_smem_bytes formula).
+// The static kernel of this problem: the BM-specialised one for X = W on the
+// equal-size grid (the §5.1 benchmark), else the runtime-dynamics kernel.
+static bool use_bm_kernel(const srmdp_t* h) {
+  return !h->jit && !h->cfg.grid && h->cfg.dyn.kind == SRMDP_DYN_BM && h->ops->step_bm;
+}
+
 static cudaError_t prepare_step(srmdp_t* h) {
+  if (use_bm_kernel(h)) return h->ops->prepare_bm(h->C, &h->smem, &h->ctas);
   if (!h->jit) return (h->cfg.grid ? h->ops->prepare_eq : h->ops->prepare)(h->C, &h->smem, &h->ctas);
   const void* k = (const void*)h->jit->step[h->cfg.grid ? 1 : 0];
   h->smem = step_smem_bytes(h->d, h->q, h->C);
@@ -512,6 +519,10 @@ static cudaError_t prepare_step(srmdp_t* h) {
 }
 
 static void launch_step(srmdp_t* h, int i, int64_t kb, int64_t nk) {
+  if (use_bm_kernel(h)) {
+    h->ops->step_bm(h->dp, i, kb, nk, h->grid, h->smem, h->stream);
+    return;
+  }
   if (!h->jit) {
     (h->cfg.grid ? h->ops->step_eq : h->ops->step)(h->dp, i, kb, nk, h->grid, h->smem, h->stream);
     return;
@@ -1280,8 +1291,8 @@ extern "C" srmdp_status srmdp_debug_trace(const srmdp_t* h, int i, int64_t k, in
 
 extern "C" srmdp_status srmdp_debug_step_dump(srmdp_t* h, int i, int dump_m, uint32_t* cell, double* x) {
   if (!h || i < 0 || i >= h->N || dump_m < 1 || dump_m > h->M || !cell || !x) return SRMDP_E_ARG;
-  if (h->jit || h->cfg.grid || !h->ops->step_dump || (h->cfg.flags & SRMDP_FLAG_LOOPBACK)) {
-    h->err = "step_dump: only the static equal-size kernels of d = q in {1, 2, 4, 6, 11, 19}";
+  if (!use_bm_kernel(h) || !h->ops->step_dump || (h->cfg.flags & SRMDP_FLAG_LOOPBACK)) {
+    h->err = "step_dump: only the static BM (X = W) equal-size kernels of d = q in {1, 2, 4, 6, 11, 19}";
     return SRMDP_E_UNSUPPORTED;
   }
   if (h->valid_from > i + 1) { h->err = "step_dump: slices i+1 .. N-1 must be present"; return SRMDP_E_STATE; }

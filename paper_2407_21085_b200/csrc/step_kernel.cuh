@@ -25,7 +25,10 @@
 
 namespace srk {
 
-constexpr int kThreads = 256;
+#ifndef SRMDP_THREADS
+#define SRMDP_THREADS 256   // threads per CTA = paths per round (A/B: build.py -DSRMDP_THREADS=128)
+#endif
+constexpr int kThreads = SRMDP_THREADS;
 
 // Kernel variants (A/B builds: build.py -DNAME=VALUE)
 #ifndef SRMDP_LDG256
@@ -35,8 +38,11 @@ constexpr int kThreads = 256;
 #define SRMDP_J_UNROLL 2   // d <= 8: path-step loop unrolled by 2, X_{j+1} / X_{j+2} swap roles without register moves (+0.9% at d = 6; at d = 19 the doubled body costs 15% in instruction-cache misses, so 1 there)
 #endif
 constexpr int kJUnroll = SRMDP_J_UNROLL;
+#ifndef SRMDP_MMA_ACC2
+#define SRMDP_MMA_ACC2 0   // measured: two DMMA chains ±0% at d = 6, -1.5% at d = 19
+#endif
 #ifndef SRMDP_PASS2_UNROLL
-#define SRMDP_PASS2_UNROLL 1   // records of several paths in flight per thread (pass 2 is latency-bound on the scratch reads)
+#define SRMDP_PASS2_UNROLL 0   // 0: the compiler's choice; n: records of several paths in flight per thread (pass 2 is latency-bound on the scratch reads)
 #endif
 constexpr int kPass2Unroll = SRMDP_PASS2_UNROLL;
 #ifndef SRMDP_PREFETCH
@@ -72,7 +78,10 @@ struct KCfg {
 #ifndef SRMDP_CTAS_LO
 #define SRMDP_CTAS_LO 3
 #endif
-  static constexpr int CTAS = (D > 8) ? 2 : SRMDP_CTAS_LO;
+#ifndef SRMDP_CTAS_HI
+#define SRMDP_CTAS_HI 2
+#endif
+  static constexpr int CTAS = (D > 8) ? SRMDP_CTAS_HI : SRMDP_CTAS_LO;
   static constexpr int S = (E <= kThreads) ? (kThreads / E) : 1;  // row slices per entry
   static constexpr int PAIRS = E * S;
   static constexpr int NACC = (PAIRS + kThreads - 1) / kThreads;
@@ -255,7 +264,7 @@ __device__ __forceinline__ void prefetch_block(const double* blk) {
 // latency, is what it costs: 256-bit instead of 128-bit loads gained 7%, an
 // explicit L1 prefetch now loses 1%. (Two paths per thread for ILP measured
 // slower: 2.43e10 vs 2.65e10.)
-template <int D, int Q, bool EQ, bool DUMP>
+template <int D, int Q, bool EQ, bool DUMP, int DK>
 __device__ __forceinline__ void simulate_path(const DevProblem& P, const Grid& G, const int (&cc)[D], int i,
                                               uint32_t k, uint32_t m, double* row, double& Bout, double& Y1out,
                                               int64_t kl) {
@@ -270,14 +279,17 @@ __device__ __forceinline__ void simulate_path(const DevProblem& P, const Grid& G
     brownian<Q>(P, G, i, i, k, m, dW);
 #pragma unroll
     for (int l = 0; l < Q; ++l) row[1 + D + l] = dW[l];
-    euler<D, Q>(P, (double)i * P.dt, Xn, dW, X1);
+    euler<D, Q, DK>(P, (double)i * P.dt, Xn, dW, X1);
 #pragma unroll
     for (int l = 0; l < D; ++l) Xn[l] = X1[l];
   }
   double acc = 0.0, zlin = 0.0, Y1 = 0.0, yv = 0.0;
   int nexact = 0;
   const int N = P.N;
-  constexpr int JU = (D <= 8) ? kJUnroll : 1;
+#ifndef SRMDP_J_UNROLL_HD
+#define SRMDP_J_UNROLL_HD 1
+#endif
+  constexpr int JU = (D <= 8) ? kJUnroll : SRMDP_J_UNROLL_HD;
 #pragma unroll JU
   for (int j = i; j < N; ++j) {
     // Xn = X_{j+1}
@@ -309,7 +321,7 @@ __device__ __forceinline__ void simulate_path(const DevProblem& P, const Grid& G
       {
         double dW[Q];
         brownian<Q>(P, G, i, j + 1, k, m, dW);   // increments of step j+1
-        euler<D, Q>(P, (double)(j + 1) * P.dt, Xn, dW, Xnn);
+        euler<D, Q, DK>(P, (double)(j + 1) * P.dt, Xn, dW, Xnn);
       }
       double a[D + 1];
       a[0] = 1.0;
@@ -481,12 +493,73 @@ __device__ void chol_solve(const double* L, const double* r, double* b) {
   }
 }
 
+// The same solve by one warp for NR right-hand sides at once (d > 8):
+// forward substitution as a wavefront -- lane q keeps row q's running sums
+// r_q - sum_{k<p} L[q][k] y_k for every right-hand side, subtracting in
+// increasing k exactly as chol_solve (bit-identical y); backward substitution
+// likewise, subtracting L[k][q] b_k for k from N1-1 down (summation order
+// differs from chol_solve at rounding level). N1 shuffle steps with NR
+// independent chains instead of an N1^2 serial chain per thread. Right-hand
+// side j is r + j*rs, its solution b + j*rs (j < nr <= NR).
+template <int N1, int NR>
+__device__ void chol_solve_warp(const double* L, const double* r, double* b, int rs, int nr, int lane) {
+  constexpr int R = (N1 + 31) / 32;
+  double s[NR][R], y[NR][R];
+#pragma unroll
+  for (int j = 0; j < NR; ++j)
+#pragma unroll
+    for (int t = 0; t < R; ++t) {
+      s[j][t] = (j < nr && lane + 32 * t < N1) ? r[j * rs + lane + 32 * t] : 0.0;
+      y[j][t] = 0.0;
+    }
+  for (int p = 0; p < N1; ++p) {
+    const double inv_owner = L[p * N1 + p];
+#pragma unroll
+    for (int j = 0; j < NR; ++j) {
+      double v = 0.0;
+#pragma unroll
+      for (int t = 0; t < R; ++t)
+        if (lane + 32 * t == p) { v = s[j][t] / inv_owner; y[j][t] = v; }
+      const double yp = __shfl_sync(0xffffffffu, v, p & 31);
+#pragma unroll
+      for (int t = 0; t < R; ++t) {
+        const int q = lane + 32 * t;
+        if (q > p && q < N1) s[j][t] = s[j][t] - L[q * N1 + p] * yp;
+      }
+    }
+  }
+  for (int p = N1 - 1; p >= 0; --p) {
+    const double lpp = L[p * N1 + p];
+#pragma unroll
+    for (int j = 0; j < NR; ++j) {
+      double v = 0.0;
+#pragma unroll
+      for (int t = 0; t < R; ++t)
+        if (lane + 32 * t == p) {
+          v = y[j][t] / lpp;
+          if (j < nr) b[j * rs + p] = v;
+        }
+      const double bp = __shfl_sync(0xffffffffu, v, p & 31);
+#pragma unroll
+      for (int t = 0; t < R; ++t) {
+        const int q = lane + 32 * t;
+        if (q < p) y[j][t] = y[j][t] - L[p * N1 + q] * bp;
+      }
+    }
+  }
+}
+
+#ifndef SRMDP_WARP_SOLVE
+#define SRMDP_WARP_SOLVE 0   // measured at d = 19: -1.5% (more code; the per-thread solves already run the q right-hand sides in parallel)
+#endif
+
 // EQ: equal-probability strata (binary-search locate) — a template parameter so
 // the equal-size grid's hot loop carries no grid branch (a runtime branch cost 4%).
 // DUMP: debug variant (srmdp_debug_step_dump) that also writes the located
 // cells and states of the first dump_m paths of every cell; otherwise the
 // same code.
-template <int D, int Q, bool EQ, bool DUMP = false>
+// DK: dynamics family fixed at compile time (-1 = runtime, see euler()).
+template <int D, int Q, bool EQ, bool DUMP = false, int DK = -1>
 __global__ void __launch_bounds__(kThreads, KCfg<D, Q>::CTAS)
 step_kernel(const DevProblem P, const int i, const int64_t k_begin, const int64_t nk) {
   using KC = KCfg<D, Q>;
@@ -581,7 +654,7 @@ step_kernel(const DevProblem P, const int i, const int64_t k_begin, const int64_
 #if SRMDP_USER_F
         simulate_path_user<D, Q, EQ>(P, G, cc, i, k, (uint32_t)m, row, Bv, Y1);
 #else
-        simulate_path<D, Q, EQ, DUMP>(P, G, cc, i, k, (uint32_t)m, row, Bv, Y1, kl);
+        simulate_path<D, Q, EQ, DUMP, DK>(P, G, cc, i, k, (uint32_t)m, row, Bv, Y1, kl);
 #endif
         const double sc = Bv * P.inv_dt;
 #pragma unroll
@@ -612,6 +685,25 @@ step_kernel(const DevProblem P, const int i, const int64_t k_begin, const int64_
             double c0 = macc[it][0], c1 = macc[it][1];
             const int rend = rhi_ < nrows ? rhi_ : nrows;
             int r0 = rlo_;
+#if SRMDP_MMA_ACC2
+            // two independent accumulator chains (even / odd k-steps of 4
+            // rows): DMMA issues back to back instead of waiting for its own
+            // previous result; summed in a fixed order below
+            double e0 = 0.0, e1 = 0.0;
+#pragma unroll 2
+            for (; r0 + 8 <= rend; r0 += 8) {
+              const double av = pa[(r0 + tig) * KC::ROW];
+              const double bv = pbp[(r0 + tig) * KC::ROW];
+              const double av2 = pa[(r0 + 4 + tig) * KC::ROW];
+              const double bv2 = pbp[(r0 + 4 + tig) * KC::ROW];
+              asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                           : "+d"(c0), "+d"(c1) : "d"(av), "d"(bv));
+              asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                           : "+d"(e0), "+d"(e1) : "d"(av2), "d"(bv2));
+            }
+            c0 = c0 + e0;
+            c1 = c1 + e1;
+#endif
 #pragma unroll 4
             for (; r0 + 4 <= rend; r0 += 4) {        // full k-steps: no predicates
               const double av = pa[(r0 + tig) * KC::ROW];
@@ -703,12 +795,19 @@ step_kernel(const DevProblem P, const int i, const int64_t k_begin, const int64_
     __syncthreads();
     const int ok = sFlag[0];
     // ---------------- solve Z ---------------------------------
-    for (int l = tid; l < Q; l += kThreads) {
-      if (ok) {
-        chol_solve<KC::N1>(sL, sRZ + l * KC::N1, sBZ + l * KC::N1);
-      } else {                                     // LP0 fallback: mean
-        sBZ[l * KC::N1] = sRZ[l * KC::N1] / (double)M;
-        for (int p = 1; p < KC::N1; ++p) sBZ[l * KC::N1 + p] = 0.0;
+    if (KC::N1 > 9 && SRMDP_WARP_SOLVE && ok) {      // d > 8: each warp solves ceil(q/8) right-hand sides at once
+      // warp w solves right-hand sides w*NRW .. w*NRW + NRW-1 together
+      constexpr int NRW = (Q + KC::NW - 1) / KC::NW;
+      const int l0 = warp * NRW, nr = (Q - l0 < NRW) ? (Q - l0) : NRW;
+      if (nr > 0) chol_solve_warp<KC::N1, NRW>(sL, sRZ + l0 * KC::N1, sBZ + l0 * KC::N1, KC::N1, nr, tid & 31);
+    } else {
+      for (int l = tid; l < Q; l += kThreads) {
+        if (ok) {
+          chol_solve<KC::N1>(sL, sRZ + l * KC::N1, sBZ + l * KC::N1);
+        } else {                                   // LP0 fallback: mean
+          sBZ[l * KC::N1] = sRZ[l * KC::N1] / (double)M;
+          for (int p = 1; p < KC::N1; ++p) sBZ[l * KC::N1 + p] = 0.0;
+        }
       }
     }
     __syncthreads();
@@ -719,14 +818,19 @@ step_kernel(const DevProblem P, const int i, const int64_t k_begin, const int64_
       double wsum = 0.0;
       for (int l = 0; l < Q; ++l) wsum = fma(zweight(P, l), sBZ[l * KC::N1 + tid], wsum);
       sW[tid] = wsum;
-    } else if (tid == KC::N1) {
+    } else if (tid >= kThreads - 32) {
+      // S by the last warp: lane l sums |beta^{Z_l}| (p ascending), then a
+      // max-reduction (fmax is exact and order-free: the serial result)
+      const int lane = tid & 31;
       double smax = 0.0;
-      for (int l = 0; l < Q; ++l) {
+      for (int l = lane; l < Q; l += 32) {
         double t = 0.0;
         for (int p = 0; p < KC::N1; ++p) t += fabs(sBZ[l * KC::N1 + p]);
         smax = fmax(smax, t);
       }
-      sS[0] = smax;
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) smax = fmax(smax, __shfl_xor_sync(0xffffffffu, smax, off));
+      if (lane == 0) sS[0] = smax;
     }
     __syncthreads();
 
@@ -734,7 +838,9 @@ step_kernel(const DevProblem P, const int i, const int64_t k_begin, const int64_
     double ry[KC::N1];
 #pragma unroll
     for (int p = 0; p < KC::N1; ++p) ry[p] = 0.0;
+#if SRMDP_PASS2_UNROLL > 0
 #pragma unroll kPass2Unroll
+#endif
     for (int64_t m = tid; m < M; m += kThreads) {
       double a[KC::N1];
       a[0] = 1.0;
@@ -796,7 +902,9 @@ step_kernel(const DevProblem P, const int i, const int64_t k_begin, const int64_
       sRY[tid] = v;
     }
     __syncthreads();
-    if (tid == 0) {
+    if (KC::N1 > 9 && SRMDP_WARP_SOLVE && ok) {
+      if (tid < 32) chol_solve_warp<KC::N1, 1>(sL, sRY, sBY, 0, 1, tid);
+    } else if (tid == 0) {
       if (ok) {
         chol_solve<KC::N1>(sL, sRY, sBY);
       } else {

@@ -49,8 +49,10 @@ def main():
         libs.append((p, L, h, keep))
     res = {p: [] for p, *_ in libs}
     steps = None
+    rng = np.random.default_rng(0)
     for r in range(a.rounds):
-        for p, L, h, _ in libs:
+        for idx in rng.permutation(len(libs)):       # build order shuffled per round (drift spreads evenly)
+            p, L, h, _ = libs[idx]
             assert L.srmdp_solve(h) == 0
             for _ in range(2):
                 assert L.srmdp_solve(h) == 0
