@@ -237,8 +237,11 @@ typedef struct {
   int grid, block, smem_bytes, ctas_per_sm; /* launch configuration of the step kernel */
   /* ABI 3: */
   uint64_t exact_z_evals;   /* path-step evaluations where the certificate (reading R23) could not rule
-                               out truncation and z was truncated per component (eq. TL) */
-  uint64_t exact_z_i;       /* the same for z_i(x_i) in the Y response (pass 2) */
+                               out truncation and z was truncated per component (eq. TL);
+                               counted by the debug kernel of srmdp_debug_step_dump only (the step it
+                               re-ran), 0 after srmdp_solve -- the count costs the d = 19 product
+                               kernel 7% even when never taken */
+  uint64_t exact_z_i;       /* the same for z_i(x_i) in the Y response (pass 2), every solve */
   double gather_ms;         /* sum of the per-step exchange durations (ncclAllGather or the fused
                                flag wait) of the last solve, device-timed (needs SRMDP_FLAG_TIME_KERNELS;
                                0 for world == 1 without FORCE_NCCL / P2P_EXCHANGE) */

@@ -29,7 +29,8 @@ srmdp_status srmdp_debug_trace(const srmdp_t* h, int i, int64_t k, int64_t m0, i
  * of every cell of this rank's range, cell[kl][m][s] = located cell of
  * X_{i+1+s} (s = 0 .. N-i-2) and x[kl][m][s][d] = X_{i+1+s} (s = 0 .. N-i-1),
  * kl = k - k_begin. Needs slices i+1 .. N-1 present; rewrites slice i with the
- * same values a solve gives. SRMDP_E_UNSUPPORTED for other (d, q) / NVRTC
+ * same values a solve gives. srmdp_stats then holds this step's event counts
+ * (lp0_fallbacks, exact_z_evals, exact_z_i). SRMDP_E_UNSUPPORTED for other (d, q) / NVRTC
  * builds / the equal-probability grid. */
 srmdp_status srmdp_debug_step_dump(srmdp_t* h, int i, int dump_m, uint32_t* cell, double* x);
 

@@ -1313,6 +1313,11 @@ extern "C" srmdp_status srmdp_debug_step_dump(srmdp_t* h, int i, int dump_m, uin
   CK(h, cudaMemcpyAsync(x, P.dump_x, nx * sizeof(double), cudaMemcpyDeviceToHost, h->stream), "dump d2h");
   if (nc) CK(h, cudaMemcpyAsync(cell, P.dump_cell, nc * sizeof(uint32_t), cudaMemcpyDeviceToHost, h->stream), "dump d2h");
   CK(h, cudaStreamSynchronize(h->stream), "step dump");
+  unsigned long long cnt[3] = {0, 0, 0};
+  CK(h, cudaMemcpy(cnt, h->d_counters, sizeof(cnt), cudaMemcpyDeviceToHost), "event counters");
+  h->st.lp0_fallbacks = cnt[0];    // of this one step
+  h->st.exact_z_evals = cnt[1];
+  h->st.exact_z_i = cnt[2];
   if (h->valid_from == i + 1) h->valid_from = i;
   h->solved = (h->valid_from == 0);
   return SRMDP_OK;

@@ -177,13 +177,16 @@ __device__ __forceinline__ double zlin_exact(const DevProblem& P, const double* 
 // Fast path (one 128-byte line for d <= 6): when S * max(1, max_p |a_p|) is
 // below C_z no component can be truncated, so zlin = W . a (same value up to
 // rounding order, reading R23); otherwise the exact per-component path.
-// Counting the exact evaluations (srmdp_stats.exact_z_evals): 1 = a
-// warp-aggregated atomic inside the exact branch, 2 = a per-thread register
-// count flushed once per path (the hot loop only increments it).
+// Counting the exact path-step evaluations (srmdp_stats.exact_z_evals) is
+// compiled into the DUMP (debug) kernels only: even never executed, the
+// counting branch in the d = 19 product kernel cost 7% (register allocation
+// of the hot loop; measured: atomic 4.72e9, register count 4.33e9, none
+// 5.05e9 path-steps/s at cfg5). 1 = a warp-aggregated atomic inside the exact
+// branch, 2 = a per-thread register count flushed once per path.
 #ifndef SRMDP_COUNT_EXACT
 #define SRMDP_COUNT_EXACT 1
 #endif
-template <int D, int Q>
+template <int D, int Q, bool COUNT>
 __device__ __forceinline__ void eval_block(const DevProblem& P, const double* __restrict__ blk,
                                            const double (&a)[D + 1], double& y, double& zlin, int& nexact) {
   using KC = KCfg<D, Q>;
@@ -231,11 +234,13 @@ __device__ __forceinline__ void eval_block(const DevProblem& P, const double* __
     zlin = wv;
   } else {
     zlin = zlin_exact<D, Q>(P, blk, a);
+    if constexpr (COUNT) {
 #if SRMDP_COUNT_EXACT == 1
-    count_event(P.counters + 1);
+      count_event(P.counters + 1);
 #elif SRMDP_COUNT_EXACT == 2
-    ++nexact;
+      ++nexact;
 #endif
+    }
   }
 }
 
@@ -327,7 +332,7 @@ __device__ __forceinline__ void simulate_path(const DevProblem& P, const Grid& G
       a[0] = 1.0;
 #pragma unroll
       for (int l = 0; l < D; ++l) a[1 + l] = Xn[l] - center_of<EQ>(P, G, c[l]);
-      eval_block<D, Q>(P, blk, a, yv, zn, nexact);   // y_{j+1}(x_{j+1}), z_{j+1}(x_{j+1})
+      eval_block<D, Q, DUMP>(P, blk, a, yv, zn, nexact);   // y_{j+1}(x_{j+1}), z_{j+1}(x_{j+1})
 #pragma unroll
       for (int l = 0; l < D; ++l) Xn[l] = Xnn[l];
     } else {
@@ -351,7 +356,7 @@ __device__ __forceinline__ void simulate_path(const DevProblem& P, const Grid& G
   Bout = yv + acc;                                 // g(x_N) + sum
   Y1out = Y1;
 #if SRMDP_COUNT_EXACT == 2
-  {   // one warp-aggregated atomic per path round
+  if constexpr (DUMP) {   // one warp-aggregated atomic per path round
     const unsigned mask = __activemask();
     const unsigned tot = __reduce_add_sync(mask, (unsigned)nexact);
     if (tot && (int)(threadIdx.x & 31) == __ffs(mask) - 1) atomicAdd(P.counters + 1, (unsigned long long)tot);
