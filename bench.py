@@ -294,8 +294,8 @@ def config_block(w, args):
             "K": w["C"] ** w["d"], "M": w["M"], "problem": "PAPER.md §5.1 benchmark (X=W, mu=1, T=1, L=6.5)"
             if w["f"] == "paper" else w["name"], "path_steps_per_solve": workloads.path_steps(w),
             "parallelism": "cells sharded over %d GPU(s), %s per time step" % (
-                args.gpus, "fused NVLink-store exchange" if getattr(args, "exchange", "nccl") == "p2p"
-                else "ncclAllGather"),
+                args.gpus, {"p2p": "fused NVLink-store exchange", "nvls": "NVLS multicast-store exchange"}.get(
+                    getattr(args, "exchange", "nccl"), "ncclAllGather")),
             "l2": "flushed (256 MB write) before every timed solve"}
 
 
@@ -309,9 +309,10 @@ def main():
     ap.add_argument("--M", type=int, default=None)
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--exchange", default="nccl", choices=["nccl", "p2p"],
-                    help="per-step slice exchange for N > 1: in-place ncclAllGather (default) or the fused "
-                         "NVLink store epilogue (SRMDP_FLAG_P2P_EXCHANGE)")
+    ap.add_argument("--exchange", default="nccl", choices=["nccl", "p2p", "nvls"],
+                    help="per-step slice exchange for N > 1: in-place ncclAllGather (default), the fused "
+                         "NVLink store epilogue (SRMDP_FLAG_P2P_EXCHANGE) or the NVLS multicast store epilogue "
+                         "(SRMDP_FLAG_NVLS_EXCHANGE)")
     ap.add_argument("--ref-path-steps", type=float, default=2.0e8)
     ap.add_argument("--no-cfg5", action="store_true", help="skip the secondary cfg5 (d = 19) block")
     ap.add_argument("--cfg5-steps", type=int, default=2)
@@ -362,7 +363,7 @@ def main():
         if world > 1:
             dist.barrier()
 
-    xflag = srmdp.FLAG_P2P_EXCHANGE if args.exchange == "p2p" else 0
+    xflag = {"nccl": 0, "p2p": srmdp.FLAG_P2P_EXCHANGE, "nvls": srmdp.FLAG_NVLS_EXCHANGE}[args.exchange]
     solver = srmdp.Solver(w, rank=rank, world=world, device=local, stream=stream.cuda_stream,
                           flags=srmdp.FLAG_TIME_KERNELS | xflag, nccl_id=nccl_id)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
@@ -412,7 +413,7 @@ def main():
             "flops_per_path_step": flops_per_path_step(w),
             "flops_per_path_start": flops_per_path_start(w),
             "kernel_share_of_step": kern_ms / total_ms, "avg_launch_ms": kern_ms / (args.steps * max(1, launches_per_solve))}
-    gather_ms = float(st["gather_ms"]) / args.steps if world > 1 or args.exchange == "p2p" else 0.0
+    gather_ms = float(st["gather_ms"]) / args.steps if world > 1 or args.exchange != "nccl" else 0.0
     solver.close()
 
     secondary = None
@@ -480,7 +481,7 @@ def main():
                     "calls": "srmdp_create+srmdp_solve+srmdp_coeffs(all i, pinned host)+srmdp_destroy"
                     if not reseed_mode else "srmdp_reseed+srmdp_solve+srmdp_coeffs(all i, pinned host) on one handle per rank"},
             # step kernels + (fused exchange) the epoch / entry-barrier kernels and a signal + wait per slice
-            "gpu_launches": (launches_per_solve + ((3 + 2 * w["N"]) if args.exchange == "p2p" else 0)) * args.steps,
+            "gpu_launches": (launches_per_solve + ((3 + 2 * w["N"]) if args.exchange in ("p2p", "nvls") else 0)) * args.steps,
             "clocks": clk.summary(),
             "lp0_fallbacks": st["lp0_fallbacks"],
             "exchange_ms_per_solve": gather_ms,

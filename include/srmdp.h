@@ -116,6 +116,15 @@ typedef struct {
                                      acquire flags at system scope order the stores against the next
                                      step's reads. NCCL is still used once, at create, to exchange
                                      the IPC handles (world > 1). */
+#define SRMDP_FLAG_NVLS_EXCHANGE 128 /* fused exchange through NVLS multicast: every
+                                     rank's [table | flags] is bound to one multicast object over the
+                                     ranks' GPUs (NVSwitch); the step kernel's epilogue stores each block
+                                     once with multimem.st and the switch writes it into every replica;
+                                     per-slice flags as P2P_EXCHANGE, published with one multimem release
+                                     store. world <= 8; NCCL serves as the rendezvous barrier (world > 1)
+                                     and the multicast handle reaches the other ranks as a file descriptor
+                                     over a Unix socket. SRMDP_E_UNSUPPORTED where the GPU / system has no
+                                     multicast. At world == 1 the multicast object spans this GPU alone. */
 #define SRMDP_FLAG_P2P_SELF_PEER 64 /* test mode of P2P_EXCHANGE at world == 1: the kernels read and store
                                      a second table on this GPU and the epilogue's peer-store loop
                                      (n_peers = 1) writes every block into the handle's own table, the

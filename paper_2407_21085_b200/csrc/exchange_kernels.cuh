@@ -34,6 +34,17 @@ __global__ void exchange_signal_kernel(const FlagPtrs F, int world, int rank, in
   asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(e) : "memory");
 }
 
+// NVLS variant: one multimem release store through the multicast mapping of
+// the flag arrays publishes the epoch at [slot][rank] in every rank's flags.
+__global__ void exchange_signal_mc_kernel(unsigned* mc_flags, int world, int rank, int slot, const unsigned* epoch) {
+  if (threadIdx.x != 0) return;
+  __threadfence_system();
+  asm volatile("fence.proxy.alias;" ::: "memory");
+  const unsigned e = *epoch;
+  unsigned* p = mc_flags + (size_t)slot * world + rank;
+  asm volatile("multimem.st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(e) : "memory");
+}
+
 // Before anything reads slice `slot` (or, for the entry slot, before the
 // first peer store): wait until every rank has published this epoch. The spin
 // is bounded (timeout_ns of %globaltimer): a rank that never signals (died,

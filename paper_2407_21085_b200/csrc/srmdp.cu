@@ -28,6 +28,7 @@
 #include "debug_kernels.cuh"
 #include "exchange_kernels.cuh"
 #include "jit.h"
+#include "nvls.h"
 #include "ops.h"
 
 using namespace srk;
@@ -292,6 +293,9 @@ struct srmdp {
   bool solved = false;
   // fused exchange (SRMDP_FLAG_P2P_EXCHANGE)
   bool p2p = false;
+  bool nvls = false;                 // SRMDP_FLAG_NVLS_EXCHANGE: table bound to a multicast object
+  NvlsTable nv;
+  unsigned* mc_flags = nullptr;      // multicast mapping of the flag arrays
   void* ipc_base = nullptr;          // cudaMalloc'd [table | flags], IPC-exported
   size_t ipc_bytes = 0;
   unsigned* d_flags = nullptr;       // own flags [N+1][world]
@@ -453,6 +457,9 @@ static srmdp_status validate(const srmdp_config* c, std::string& err) {
     return bad(SRMDP_E_ARG, "P2P_EXCHANGE needs world <= 8 and excludes LOOPBACK");
   if ((c->flags & SRMDP_FLAG_P2P_SELF_PEER) && (!(c->flags & SRMDP_FLAG_P2P_EXCHANGE) || c->world != 1))
     return bad(SRMDP_E_ARG, "P2P_SELF_PEER is a world == 1 test mode of P2P_EXCHANGE");
+  if ((c->flags & SRMDP_FLAG_NVLS_EXCHANGE) &&
+      (loopback || (c->flags & SRMDP_FLAG_P2P_EXCHANGE) || c->world > kMaxRanks))
+    return bad(SRMDP_E_ARG, "NVLS_EXCHANGE needs world <= 8 and excludes LOOPBACK and P2P_EXCHANGE");
   if (c->dyn.kind < 0 || c->dyn.kind > 4 || c->driver.kind < 0 || c->driver.kind > 3 || c->terminal.kind < 0 ||
       c->terminal.kind > 2)
     return bad(SRMDP_E_ARG, "unknown problem family kind");
@@ -538,11 +545,12 @@ static srmdp_status enqueue_sweep(srmdp_t* h, int i_hi, int i_lo) {
   const int64_t nk = h->k_end - h->k_begin;
   const bool loopback = h->cfg.flags & SRMDP_FLAG_LOOPBACK;
   h->launches_per_solve = 0;
-  if (h->p2p) {
+  if (h->p2p || h->nvls) {
     // new epoch; entry barrier: no rank stores into a peer's table before
     // that peer has entered this sweep (slot N)
     epoch_kernel<<<1, 1, 0, h->stream>>>(h->d_epoch);
-    exchange_signal_kernel<<<1, kMaxRanks, 0, h->stream>>>(h->fptr, h->cfg.world, h->cfg.rank, h->N, h->d_epoch);
+    if (h->nvls) exchange_signal_mc_kernel<<<1, 32, 0, h->stream>>>(h->mc_flags, h->cfg.world, h->cfg.rank, h->N, h->d_epoch);
+    else exchange_signal_kernel<<<1, kMaxRanks, 0, h->stream>>>(h->fptr, h->cfg.world, h->cfg.rank, h->N, h->d_epoch);
     exchange_wait_kernel<<<1, kMaxRanks, 0, h->stream>>>(h->d_flags, h->cfg.world, h->N, h->d_epoch, h->d_xerr,
                                                          h->xchg_timeout_ns);
     CK(h, cudaGetLastError(), "exchange entry barrier");
@@ -568,11 +576,12 @@ static srmdp_status enqueue_sweep(srmdp_t* h, int i_hi, int i_lo) {
     }
     CK(h, cudaGetLastError(), "step kernel launch");
     if (timed) CK(h, record_event(h, h->ev[2 * i + 1]), "event");
-    const bool xchg = h->p2p || h->comm;
+    const bool xchg = h->p2p || h->nvls || h->comm;
     if (timed && xchg) CK(h, record_event(h, h->ev[2 * h->N + 2 * i]), "event");
-    if (h->p2p) {
+    if (h->p2p || h->nvls) {
       // blocks of slice i are in every table once all ranks have signalled
-      exchange_signal_kernel<<<1, kMaxRanks, 0, h->stream>>>(h->fptr, h->cfg.world, h->cfg.rank, i, h->d_epoch);
+      if (h->nvls) exchange_signal_mc_kernel<<<1, 32, 0, h->stream>>>(h->mc_flags, h->cfg.world, h->cfg.rank, i, h->d_epoch);
+      else exchange_signal_kernel<<<1, kMaxRanks, 0, h->stream>>>(h->fptr, h->cfg.world, h->cfg.rank, i, h->d_epoch);
       exchange_wait_kernel<<<1, kMaxRanks, 0, h->stream>>>(h->d_flags, h->cfg.world, i, h->d_epoch, h->d_xerr,
                                                            h->xchg_timeout_ns);
       CK(h, cudaGetLastError(), "exchange flags");
@@ -659,6 +668,7 @@ extern "C" srmdp_status srmdp_create(const srmdp_config* cfg, srmdp_t** out) {
   const size_t table_bytes = (size_t)h->N * h->K_pad * h->B_pad * sizeof(double);
   std::vector<double> tabs = grid_tables(h->C, cfg->L, cfg->mu, cfg->grid != 0);
   h->p2p = cfg->flags & SRMDP_FLAG_P2P_EXCHANGE;
+  h->nvls = cfg->flags & SRMDP_FLAG_NVLS_EXCHANGE;
   {   // bounded flag waits of the fused exchange (exchange_wait_kernel)
     const char* t = getenv("SRMDP_EXCHANGE_TIMEOUT_S");
     const double sec = (t && atof(t) > 0) ? atof(t) : 60.0;
@@ -680,6 +690,14 @@ extern "C" srmdp_status srmdp_create(const srmdp_config* cfg, srmdp_t** out) {
     h->d_table = (double*)h->ipc_base;
     h->d_flags = (unsigned*)((char*)h->ipc_base + flags_off);
     h->fptr.f[cfg->rank] = h->d_flags;
+  } else if (h->nvls) {   // the table comes from nvls_create below (after the communicator exists)
+    if ((e = dalloc(h, &h->d_epoch, sizeof(unsigned))) != cudaSuccess ||
+        (e = cudaMemsetAsync(h->d_epoch, 0, sizeof(unsigned), h->stream)) != cudaSuccess ||
+        (e = dalloc(h, &h->d_xerr, sizeof(unsigned))) != cudaSuccess ||
+        (e = cudaMemsetAsync(h->d_xerr, 0, sizeof(unsigned), h->stream)) != cudaSuccess) {
+      cuda_fail(h, e, "nvls flag alloc");
+      return fail(SRMDP_E_NOMEM);
+    }
   } else if ((e = dalloc(h, &h->d_table, table_bytes)) != cudaSuccess) {
     cuda_fail(h, e, "table alloc");
     return fail(SRMDP_E_NOMEM);
@@ -777,6 +795,39 @@ extern "C" srmdp_status srmdp_create(const srmdp_config* cfg, srmdp_t** out) {
     ncclResult_t r = api.CommInitRank(&h->comm, cfg->world, id, cfg->rank);
     if (r != ncclSuccess) { h->err = std::string("ncclCommInitRank: ") + api.GetErrorString(r); return fail(SRMDP_E_NCCL); }
   }
+  if (h->nvls) {
+    // [table | flags] bound to a multicast object over the ranks' GPUs (nvls.h);
+    // the communicator serves as the rendezvous barrier
+    char* bar = nullptr;
+    if ((e = dalloc(h, &bar, 16 * cfg->world)) != cudaSuccess) { cuda_fail(h, e, "nvls barrier"); return fail(SRMDP_E_NOMEM); }
+    auto barrier = [&]() -> bool {
+      if (!h->comm) return true;
+      if (nccl().AllGather(bar, bar, 16, ncclChar, h->comm, h->stream) != ncclSuccess) return false;
+      return cudaStreamSynchronize(h->stream) == cudaSuccess;
+    };
+    std::string key;
+    if (cfg->world > 1) {
+      uint64_t kh = 0xcbf29ce484222325ull;
+      const unsigned char* u = (const unsigned char*)cfg->nccl_unique_id;
+      for (int t = 0; t < 128; ++t) { kh ^= u[t]; kh *= 0x100000001b3ull; }
+      char buf[32];
+      snprintf(buf, sizeof(buf), "%016llx", (unsigned long long)kh);
+      key = buf;
+    }
+    std::string nerr;
+    const bool ok = nvls_create(cfg->device, flags_off + flags_bytes, cfg->world, cfg->rank, key, barrier, &h->nv, nerr);
+    if (ok) {
+      h->d_table = (double*)h->nv.uc;
+      h->d_flags = (unsigned*)((char*)h->nv.uc + flags_off);
+      h->mc_flags = (unsigned*)((char*)h->nv.mc + flags_off);
+      e = cudaMemsetAsync(h->d_flags, 0, flags_bytes, h->stream);
+    }
+    const bool ok2 = ok && e == cudaSuccess && barrier();   // every rank's flags zeroed before anyone signals
+    dfree(h, bar);
+    if (!ok2) { h->err = ok ? "nvls flag init" : nerr; return fail(ok ? SRMDP_E_CUDA : SRMDP_E_UNSUPPORTED); }
+    h->dp.table = h->d_table;
+    h->dp.mc_table = (double*)h->nv.mc;
+  }
   if (h->p2p && cfg->world > 1) {
     // exchange the IPC handles of [table | flags] over the communicator, open the peers'
     if (!h->comm) { h->err = "P2P_EXCHANGE with world > 1 needs nccl_unique_id"; return fail(SRMDP_E_ARG); }
@@ -872,7 +923,7 @@ static srmdp_status finish_solve(srmdp_t* h, std::chrono::steady_clock::time_poi
   if (se != cudaSuccess) return cuda_fail(h, se, "solve");
   unsigned long long cnt[3] = {0, 0, 0};
   CK(h, cudaMemcpy(cnt, h->d_counters, sizeof(cnt), cudaMemcpyDeviceToHost), "event counters");
-  if (h->p2p) {
+  if (h->p2p || h->nvls) {
     unsigned xerr = 0;
     CK(h, cudaMemcpy(&xerr, h->d_xerr, sizeof(xerr), cudaMemcpyDeviceToHost), "exchange status");
     if (xerr) {
@@ -897,7 +948,7 @@ static srmdp_status finish_solve(srmdp_t* h, std::chrono::steady_clock::time_poi
       CK(h, cudaEventElapsedTime(&ms, h->ev[2 * i], h->ev[2 * i + 1]), "event time");
       h->step_ms[i] = ms;
       tot += ms;
-      if (h->p2p || h->comm) {
+      if (h->p2p || h->nvls || h->comm) {
         CK(h, cudaEventElapsedTime(&ms, h->ev[2 * h->N + 2 * i], h->ev[2 * h->N + 2 * i + 1]), "event time");
         h->xchg_ms[i] = ms;
         xt += ms;
@@ -1187,6 +1238,11 @@ extern "C" void srmdp_destroy(srmdp_t* h) {
   if (h->ipc_base) {
     if (h->stream) cudaStreamSynchronize(h->stream);
     ipc_release(h->cfg.device, h->ipc_base, h->ipc_bytes);
+    h->d_table = nullptr;
+  }
+  if (h->nvls) {
+    if (h->stream) cudaStreamSynchronize(h->stream);
+    nvls_destroy(&h->nv);
     h->d_table = nullptr;
   }
   if (h->stream) {

@@ -927,12 +927,20 @@ step_kernel(const DevProblem P, const int i, const int64_t k_begin, const int64_
       else if (b < 2 * KC::N1) v = sW[b - KC::N1];
       else if (b == 2 * KC::N1) v = sS[0];
       else if (b >= KC::NH && b < KC::NH + KC::NZ) v = sBZ[b - KC::NH];
-      dst[b] = v;
+      if (P.mc_table) {
+        // NVLS exchange: one multimem store through the multicast mapping;
+        // NVSwitch writes it into every rank's replica (this one included)
+        asm volatile("multimem.st.relaxed.sys.global.f64 [%0], %1;" ::"l"(P.mc_table + (dst - P.table) + b), "d"(v)
+                     : "memory");
+      } else {
+        dst[b] = v;
+      }
       // fused exchange: the same block into every peer's replica (NVLink
       // stores, coalesced per block); made visible by exchange_signal_kernel
       for (int r = 0; r < P.n_peers; ++r) P.peer_table[r][(dst - P.table) + b] = v;
     }
-    if (P.n_peers) __threadfence_system();   // peer stores ordered before the signal kernel's release
+    if (P.mc_table) asm volatile("fence.proxy.alias;" ::: "memory");   // multicast alias vs the unicast reads
+    if (P.n_peers || P.mc_table) __threadfence_system();   // ordered before the signal kernel's release
     __syncthreads();
   }
 }

@@ -44,15 +44,38 @@ int main() {
     return 0;
   }
   CUmulticastObjectProp mp;
-  memset(&mp, 0, sizeof(mp));
-  mp.numDevices = 1;
-  mp.handleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;
-  size_t gran = 0;
-  mp.size = 2 << 20;
-  CU(cuMulticastGetGranularity(&gran, &mp, CU_MULTICAST_GRANULARITY_RECOMMENDED));
-  const size_t size = ((size_t)(4 << 20) + gran - 1) / gran * gran;
-  mp.size = size;
-  CUmemGenericAllocationHandle mc;
+  size_t gran = 0, size = 0;
+  CUmemGenericAllocationHandle mc = 0;
+  {   // which (numDevices, handle type) combinations does this system accept?
+    const int nds[2] = {1, 2};
+    const unsigned long long hts[3] = {0, CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR, CU_MEM_HANDLE_TYPE_FABRIC};
+    for (int a = 0; a < 2; ++a)
+      for (int b = 0; b < 3; ++b) {
+        memset(&mp, 0, sizeof(mp));
+        mp.numDevices = nds[a];
+        mp.handleTypes = hts[b];
+        mp.size = 2 << 20;
+        size_t g = 0, gm = 0;
+        CUresult r1 = cuMulticastGetGranularity(&g, &mp, CU_MULTICAST_GRANULARITY_RECOMMENDED);
+        cuMulticastGetGranularity(&gm, &mp, CU_MULTICAST_GRANULARITY_MINIMUM);
+        mp.size = g ? g : (2 << 20);
+        CUmemGenericAllocationHandle h = 0;
+        CUresult r2 = cuMulticastCreate(&h, &mp);
+        const char* s2 = nullptr;
+        cuGetErrorString(r2, &s2);
+        fprintf(stderr, "numDevices=%d handleTypes=%llu gran=%zu (min %zu, r=%d) create=%s\n", nds[a], hts[b], g, gm,
+                (int)r1, s2 ? s2 : "?");
+        if (r2 == CUDA_SUCCESS) {
+          if (!mc && nds[a] == 1) { mc = h; gran = g; size = g * 2; mp.size = size; }
+          else cuMemRelease(h);
+        }
+      }
+  }
+  if (!mc) {
+    printf("{\"ok\": false, \"step\": \"cuMulticastCreate\", \"error\": \"no accepted combination for one device (see stderr)\"}\n");
+    return 1;
+  }
+  cuMemRelease(mc);
   CU(cuMulticastCreate(&mc, &mp));
   CU(cuMulticastAddDevice(mc, dev));
 
@@ -61,7 +84,7 @@ int main() {
   ap.type = CU_MEM_ALLOCATION_TYPE_PINNED;
   ap.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
   ap.location.id = 0;
-  ap.requestedHandleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;
+  ap.requestedHandleTypes = (CUmemAllocationHandleType)mp.handleTypes;
   CUmemGenericAllocationHandle ph;
   CU(cuMemCreate(&ph, size, &ap, 0));
   CU(cuMulticastBindMem(mc, 0, ph, 0, size, 0));
