@@ -748,6 +748,7 @@ extern "C" srmdp_status srmdp_create(const srmdp_config* cfg, srmdp_t** out) {
   P.L = cfg->L;
   P.inv_delta = (double)h->C / (2.0 * cfg->L);
   P.delta = (2.0 * cfg->L) / (double)h->C;     // as grid_tables (centers)
+  P.half_delta = P.delta * 0.5;
   P.neg_inv_mu = -(1.0 / cfg->mu);
   P.C_y = h->C_y; P.C_z = h->C_z;
   P.f_a = (cfg->driver.kind == SRMDP_F_LINEAR) ? cfg->driver.params[0] : 0.0;

@@ -38,6 +38,9 @@ constexpr int kThreads = SRMDP_THREADS;
 #define SRMDP_J_UNROLL 2   // d <= 8: path-step loop unrolled by 2, X_{j+1} / X_{j+2} swap roles without register moves (+0.9% at d = 6; at d = 19 the doubled body costs 15% in instruction-cache misses, so 1 there)
 #endif
 constexpr int kJUnroll = SRMDP_J_UNROLL;
+#ifndef SRMDP_LOCATE_MAGIC
+#define SRMDP_LOCATE_MAGIC 0
+#endif
 #ifndef SRMDP_MMA_ACC2
 #define SRMDP_MMA_ACC2 0   // measured: two DMMA chains ±0% at d = 6, -1.5% at d = 19
 #endif
@@ -302,10 +305,35 @@ __device__ __forceinline__ void simulate_path(const DevProblem& P, const Grid& G
     if (j + 1 < N) {
       int c[D];
       uint32_t kn = 0;
+#if SRMDP_LOCATE_MAGIC
+      if constexpr (!EQ) {
+        // floor((x + L) / delta) without a conversion instruction: rounded
+        // down, t + 1.5*2^52 is 1.5*2^52 + floor(t) exactly for |t| < 2^51, so
+        // the low word is floor(t) whenever the high word shows |t| < 2^31
+        // (else -- NaN, inf, huge x -- every coordinate takes locate1); the
+        // same cells as locate1 (docs/streams.md §6) for every input
+        unsigned bad = 0;
 #pragma unroll
-      for (int l = 0; l < D; ++l) {
-        c[l] = locate_g<EQ>(P, G.edge, Xn[l]);
-        kn = kn * (uint32_t)P.C + (uint32_t)c[l];
+        for (int l = 0; l < D; ++l) {
+          const double t = __dmul_rn(__dadd_rn(Xn[l], P.L), P.inv_delta);
+          const double r = __dadd_rd(t, 0x1.8p52);
+          bad |= (unsigned)(__double2hiint(r) - 0x4337ffff) > 1u ? 1u : 0u;
+          c[l] = min(max(__double2loint(r), 0), P.C - 1);
+        }
+        if (bad) {
+#pragma unroll
+          for (int l = 0; l < D; ++l) c[l] = locate1(Xn[l], P.L, P.inv_delta, P.C);
+        }
+#pragma unroll
+        for (int l = 0; l < D; ++l) kn = kn * (uint32_t)P.C + (uint32_t)c[l];
+      } else
+#endif
+      {
+#pragma unroll
+        for (int l = 0; l < D; ++l) {
+          c[l] = locate_g<EQ>(P, G.edge, Xn[l]);
+          kn = kn * (uint32_t)P.C + (uint32_t)c[l];
+        }
       }
 #ifdef SRMDP_EXPERIMENT_GATHER_SELF   // timing experiment only (wrong results): every gather hits the start cell
       kn = k;

@@ -117,3 +117,18 @@ def test_create_validation_needs_no_gpu(lib):
     with pytest.raises(lib.SrmdpError) as e:           # P2P exchange excludes loopback
         lib.Solver(base, world=2, flags=lib.FLAG_LOOPBACK | lib.FLAG_P2P_EXCHANGE)
     assert e.value.status == -1
+
+
+def test_exchange_flag_validation_needs_no_gpu(lib):
+    """The fused-exchange modes reject inconsistent flag sets before any CUDA
+    call (include/srmdp.h: P2P_SELF_PEER is a world == 1 test mode of
+    P2P_EXCHANGE; NVLS_EXCHANGE excludes LOOPBACK and P2P_EXCHANGE)."""
+    import workloads
+    base = workloads.benchmark(d=2, N=3, C=3, M=10)
+    for flags, world, msg in ((lib.FLAG_P2P_SELF_PEER, 1, "P2P_SELF_PEER"),
+                              (lib.FLAG_P2P_EXCHANGE | lib.FLAG_P2P_SELF_PEER, 2, "P2P_SELF_PEER"),
+                              (lib.FLAG_NVLS_EXCHANGE | lib.FLAG_P2P_EXCHANGE, 1, "NVLS_EXCHANGE"),
+                              (lib.FLAG_NVLS_EXCHANGE | lib.FLAG_LOOPBACK, 2, "NVLS_EXCHANGE")):
+        with pytest.raises(lib.SrmdpError) as e:
+            lib.Solver(base, world=world, rank=0, flags=flags, nccl_id=b"x" * 128 if world > 1 else None)
+        assert e.value.status == -1 and msg in str(e.value), (flags, str(e.value))
