@@ -41,6 +41,9 @@ constexpr int kJUnroll = SRMDP_J_UNROLL;
 #ifndef SRMDP_LOCATE_MAGIC
 #define SRMDP_LOCATE_MAGIC 0
 #endif
+#ifndef SRMDP_MMA_REUSE
+#define SRMDP_MMA_REUSE 0
+#endif
 #ifndef SRMDP_MMA_ACC2
 #define SRMDP_MMA_ACC2 0   // measured: two DMMA chains ±0% at d = 6, -1.5% at d = 19
 #endif
@@ -116,6 +119,26 @@ struct KCfg {
   static constexpr bool BAL_FITS = TILES * KSPLIT_BAL * 64 + SOLVE_LEN + 2 <= ROWS * row_stride(D, Q);
   static constexpr int KSPLIT = (SRMDP_KSPLIT_BALANCE && BAL_FITS) ? KSPLIT_BAL : KSPLIT_OLD;
   static constexpr int ITEMS = TILES * KSPLIT;      // (tile, row slice) work items
+  // Fragment-reusing fold (SRMDP_MMA_REUSE): warp w takes one tile row pb
+  // (all QB - pb tiles of it) over a row slice, so each 8-column fragment is
+  // loaded once per k-step for every tile of the row (QB - pb loads for QB - pb
+  // DMMA instead of 2 per DMMA). Warps per tile row in proportion to its
+  // tiles (largest remainder, at least one each).
+  __host__ __device__ static constexpr int GT(int p) { return QB - p; }
+  __host__ __device__ static constexpr int GW(int p) {               // warps of tile row p
+    int n[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    int used = 0;
+    for (int g = 0; g < PB; ++g) { n[g] = (NW * GT(g)) / TILES; if (n[g] < 1) n[g] = 1; used += n[g]; }
+    while (used < NW) {                          // largest remainder NW*GT/TILES - n
+      int best = 0, bv = -1000000;
+      for (int g = 0; g < PB; ++g) { const int r = NW * GT(g) - n[g] * TILES; if (r > bv) { bv = r; best = g; } }
+      ++n[best]; ++used;
+    }
+    return n[p];
+  }
+  __host__ __device__ static constexpr int GW0(int p) { int f = 0; for (int g = 0; g < p; ++g) f += GW(g); return f; }        // first warp
+  __host__ __device__ static constexpr int GSLOT(int p) { int f = 0; for (int g = 0; g < p; ++g) f += GT(g) * GW(g); return f; }  // first partial slot
+  static constexpr int RSLOTS = GSLOT(PB);       // (tile, slice) partials of the reuse fold
   static constexpr int NI = (ITEMS + NW - 1) / NW;  // items per warp
   // odd row stride (spreads banks); MMA fragment loads of the padding columns
   // (>= NCOL) read neighbouring smem and only feed discarded outputs
@@ -132,12 +155,13 @@ struct SmemLayout {
   // d = 6 CTA at 31 KB, so 3 CTAs/SM fit a 100 KB shared-memory carveout and
   // L1 keeps the rest for the coefficient hot lines (fit_carveout, ops.h).
   using KC = KCfg<D, Q>;
-  static constexpr int RED = (((KC::USE_MMA ? KC::ITEMS * 64 : KC::PAIRS) > kThreads
-                                   ? (KC::USE_MMA ? KC::ITEMS * 64 : KC::PAIRS)
+  static constexpr int MMA_RED = (SRMDP_MMA_REUSE ? KC::RSLOTS : KC::ITEMS) * 64;
+  static constexpr int RED = (((KC::USE_MMA ? MMA_RED : KC::PAIRS) > kThreads
+                                   ? (KC::USE_MMA ? MMA_RED : KC::PAIRS)
                                    : kThreads) + 1) & ~1;
   static constexpr int SOLVE = KC::SOLVE_LEN;
   static_assert(RED + SOLVE <= KC::ROWS * KC::ROW, "solve arrays must fit in the row tile");
-  static_assert(!KC::USE_MMA || KC::ITEMS * 64 <= RED, "MMA tile partials must fit the reduction scratch");
+  static_assert(!KC::USE_MMA || MMA_RED <= RED, "MMA tile partials must fit the reduction scratch");
   static_assert(!KC::USE_MMA || 8 * (KC::QB - 1) + 7 < KC::ROW + 8, "MMA fragment columns stay within a row + padding");
   __host__ __device__ static int tabs(int C) { return smem_tabs_len(D, C); }
   __host__ __device__ static int rows(int C) { return tabs(C); }
@@ -675,9 +699,10 @@ step_kernel(const DevProblem P, const int i, const int64_t k_begin, const int64_
     double acc[KC::NACC];
 #pragma unroll
     for (int n = 0; n < KC::NACC; ++n) acc[n] = 0.0;
-    double macc[KC::NI][2];
+    constexpr int NMACC = SRMDP_MMA_REUSE ? KC::QB : KC::NI;
+    double macc[NMACC][2];
 #pragma unroll
-    for (int it = 0; it < KC::NI; ++it) macc[it][0] = macc[it][1] = 0.0;
+    for (int it = 0; it < NMACC; ++it) macc[it][0] = macc[it][1] = 0.0;
     for (int64_t m0 = 0; m0 < M; m0 += KC::ROWS) {
       const int nrows = (int)((M - m0) < KC::ROWS ? (M - m0) : KC::ROWS);
       const int64_t m = m0 + tid;
@@ -701,7 +726,32 @@ step_kernel(const DevProblem P, const int i, const int64_t k_begin, const int64_
         }
       }
       __syncthreads();
-      if constexpr (KC::USE_MMA) {
+      if constexpr (KC::USE_MMA && SRMDP_MMA_REUSE) {
+        // fragment-reusing fold: this warp's tile row pb over its row slice
+        int pb = 0;
+#pragma unroll
+        for (int g = 1; g < KC::PB; ++g) pb += (warp >= KC::GW0(g)) ? 1 : 0;
+        int nw = 0, w0 = 0, nt = 0;
+#pragma unroll
+        for (int g = 0; g < KC::PB; ++g)
+          if (g == pb) { nw = KC::GW(g); w0 = KC::GW0(g); nt = KC::GT(g); }
+        const int sl = warp - w0;
+        const int rlo_ = 4 * ((sl * (kThreads / 4)) / nw), rhi_ = 4 * (((sl + 1) * (kThreads / 4)) / nw);
+        const int rend = rhi_ < nrows ? rhi_ : nrows;
+        const double* pf = sRows + 8 * pb + gid;    // fragment t: columns 8 (pb + t) .. + 7
+        for (int r0 = rlo_; r0 < rend; r0 += 4) {
+          const int rr = r0 + tig;
+          const bool in = rr < rend;                 // ragged last k-step: rows >= nrows are 0
+          double f[KC::QB];
+#pragma unroll
+          for (int t = 0; t < KC::QB; ++t) f[t] = (t < nt && in) ? pf[rr * KC::ROW + 8 * t] : 0.0;
+#pragma unroll
+          for (int t = 0; t < KC::QB; ++t)
+            if (t < nt)
+              asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                           : "+d"(macc[t][0]), "+d"(macc[t][1]) : "d"(f[0]), "d"(f[t]));
+        }
+      } else if constexpr (KC::USE_MMA) {
         // C += V^T V on the tensor cores: A(8x4) = V[r0..r0+3][p0..p0+7]^T,
         // B(4x8) = V[r0..r0+3][q0..q0+7]; rows >= nrows contribute 0
 #pragma unroll
@@ -766,7 +816,46 @@ step_kernel(const DevProblem P, const int i, const int64_t k_begin, const int64_
       }
       __syncthreads();
     }
-    if constexpr (KC::USE_MMA) {
+    if constexpr (KC::USE_MMA && SRMDP_MMA_REUSE) {
+      // partials -> shared memory [slot][8][8], slot = GSLOT(pb) + t * GW(pb) + slice;
+      // then a fixed-order sum over the slices of each tile
+      double* red = sRows;
+      {
+        int pb = 0;
+#pragma unroll
+        for (int g = 1; g < KC::PB; ++g) pb += (warp >= KC::GW0(g)) ? 1 : 0;
+#pragma unroll
+        for (int g = 0; g < KC::PB; ++g)
+          if (g == pb) {
+            const int sl = warp - KC::GW0(g);
+#pragma unroll
+            for (int t = 0; t < KC::QB; ++t)
+              if (t < KC::GT(g)) {
+                const int slot = KC::GSLOT(g) + t * KC::GW(g) + sl;
+                red[slot * 64 + gid * 8 + 2 * tig] = macc[t][0];
+                red[slot * 64 + gid * 8 + 2 * tig + 1] = macc[t][1];
+              }
+          }
+      }
+      __syncthreads();
+      for (int e = tid; e < KC::N1 * KC::NCOL; e += kThreads) {
+        const int p = e / KC::NCOL, q2 = e % KC::NCOL;
+        if (q2 < p) continue;                       // Gram: upper half only
+        const int pb = p / 8, t = q2 / 8 - pb;
+        int nw = 0, s0 = 0;
+#pragma unroll
+        for (int g = 0; g < KC::PB; ++g)
+          if (g == pb) { nw = KC::GW(g); s0 = KC::GSLOT(g) + t * KC::GW(g); }
+        double v = red[s0 * 64 + (p % 8) * 8 + (q2 % 8)];
+        for (int sl = 1; sl < nw; ++sl) v = v + red[(s0 + sl) * 64 + (p % 8) * 8 + (q2 % 8)];
+        if (q2 < KC::N1) {
+          sL[p * KC::N1 + q2] = v;
+          sL[q2 * KC::N1 + p] = v;
+        } else {
+          sRZ[(q2 - KC::N1) * KC::N1 + p] = v;      // [l][p]
+        }
+      }
+    } else if constexpr (KC::USE_MMA) {
       // tile partials -> shared memory [item][8][8], then fixed-order sum over row slices
       double* red = sRows;
 #pragma unroll
