@@ -272,6 +272,29 @@ srmdp_status srmdp_shard_plan(int64_t K, int world, int rank, int64_t out[4]);
 srmdp_status srmdp_jit_check(int d, int q, int dyn_kind, int f_kind, int g_kind, const char* user_src, char* log,
                              size_t log_len);
 
+/* Parameter planner of the paper's complexity analysis (§4.3) --
+ * pure host arithmetic, no GPU. For a target of O(1/N) total error:
+ *   L = log(N)/mu                         (nu(R^d \ [-L,L]^d) <= 2d e^{-mu L} = O(1/N))
+ *   delta = c_delta N^{-1/4} (LP1) or c_delta N^{-1/2} (LP0)   (squared bias delta^4 resp. delta^2)
+ *   cells_per_dim = max(1, ceil(2L / delta)),  K = cells_per_dim^d     (K = O(N^{d/4}) resp. O(N^{d/2}))
+ *   M = ceil(c_M (d+1) N^2) (LP1) or ceil(c_M N^2) (LP0)   (statistical error O(N K' log M / M))
+ * and reports what that costs on this implementation: the replicated
+ * coefficient table N K B_pad 8 bytes (docs/layout.md), path-steps
+ * K M N(N+1)/2 and path-starts K M N per solve (the computational cost
+ * O(N^{4+d/4}) resp. O(N^{4+d/2})), and whether the table fits
+ * `mem_bytes` (e.g. 180e9 per B200; 0 = no check). c_delta, c_M <= 0 mean 1. */
+typedef struct {
+  double L, delta;
+  int cells_per_dim;
+  int64_t K, M;
+  int B, B_pad;
+  double table_bytes;       /* N * K * B_pad * 8 */
+  double path_steps, path_starts;
+  int fits;                 /* table_bytes <= mem_bytes (1 when mem_bytes == 0) */
+} srmdp_plan_t;
+srmdp_status srmdp_plan(int d, int q, int N, double mu, int lp0, double c_delta, double c_M, double mem_bytes,
+                        srmdp_plan_t* out);
+
 /* Library version / build info string (ABI version, arch, compiled (d,q)). */
 const char* srmdp_build_info(void);
 

@@ -13,6 +13,8 @@
 #include <nvtx3/nvToolsExt.h>   // header-only NVTX v3: ranges cost nothing without a tool attached
 
 #include <chrono>
+#include <algorithm>
+#include <climits>
 #include <cmath>
 #include <map>
 #include <mutex>
@@ -1302,6 +1304,30 @@ extern "C" srmdp_status srmdp_jit_check(int d, int q, int dyn_kind, int f_kind, 
     log[n] = '\0';
   }
   return ok ? SRMDP_OK : SRMDP_E_JIT;
+}
+
+extern "C" srmdp_status srmdp_plan(int d, int q, int N, double mu, int lp0, double c_delta, double c_M,
+                                   double mem_bytes, srmdp_plan_t* out) {
+  if (!out || d < 1 || q < 1 || d > 32 || q > 32 || N < 1 || !(mu > 0) || mem_bytes < 0) return SRMDP_E_ARG;
+  const double cd = c_delta > 0 ? c_delta : 1.0, cm = c_M > 0 ? c_M : 1.0;
+  srmdp_plan_t p{};
+  p.L = std::log((double)N) / mu;
+  p.delta = cd * std::pow((double)N, lp0 ? -0.5 : -0.25);
+  const double cpd = std::ceil(2.0 * p.L / p.delta);
+  p.cells_per_dim = (p.L > 0 && cpd >= 1) ? (int)std::min(cpd, 2048.0) : 1;
+  double K = 1;
+  for (int l = 0; l < d; ++l) K *= p.cells_per_dim;
+  p.K = K < 9.2e18 ? (int64_t)K : INT64_MAX;
+  const double M = std::ceil(cm * (lp0 ? 1.0 : (double)(d + 1)) * (double)N * (double)N);
+  p.M = (int64_t)std::max(M, (double)(d + 1));
+  p.B = (q + 1) * (d + 1);
+  p.B_pad = block_stride(d, q);
+  p.table_bytes = (double)N * K * (double)p.B_pad * 8.0;
+  p.path_steps = K * (double)p.M * (double)N * (double)(N + 1) / 2.0;
+  p.path_starts = K * (double)p.M * (double)N;
+  p.fits = (mem_bytes == 0 || p.table_bytes <= mem_bytes) ? 1 : 0;
+  *out = p;
+  return SRMDP_OK;
 }
 
 extern "C" const char* srmdp_build_info(void) {

@@ -72,6 +72,13 @@ class srmdp_stats_t(ctypes.Structure):
     ]
 
 
+class srmdp_plan_t(ctypes.Structure):
+    _fields_ = [("L", ctypes.c_double), ("delta", ctypes.c_double), ("cells_per_dim", ctypes.c_int),
+                ("K", ctypes.c_int64), ("M", ctypes.c_int64), ("B", ctypes.c_int), ("B_pad", ctypes.c_int),
+                ("table_bytes", ctypes.c_double), ("path_steps", ctypes.c_double), ("path_starts", ctypes.c_double),
+                ("fits", ctypes.c_int)]
+
+
 _lib = None
 _PD = ctypes.POINTER(ctypes.c_double)
 _P64 = ctypes.POINTER(ctypes.c_int64)
@@ -98,6 +105,8 @@ SIGNATURES = {
     "srmdp_stats": (ctypes.c_int, [_H, ctypes.POINTER(srmdp_stats_t)]),
     "srmdp_shard_plan": (ctypes.c_int, [ctypes.c_int64, ctypes.c_int, ctypes.c_int, _P64]),
     "srmdp_build_info": (ctypes.c_char_p, []),
+    "srmdp_plan": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_double, ctypes.c_int,
+                                  ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.POINTER(srmdp_plan_t)]),
     "srmdp_jit_check": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                        ctypes.c_char_p, ctypes.c_char_p, ctypes.c_size_t]),
     "srmdp_debug_trace": (ctypes.c_int, [_H, ctypes.c_int, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, _PD, _P64, _PD]),
@@ -150,6 +159,14 @@ def srmdp_jit_check(d: int, q: int, dyn: str, f: str, g: str, user_src: str | No
     if st == -1:
         raise SrmdpError(st, "d, q must be in 1..32")
     return st == 0, buf.value.decode()
+
+
+def srmdp_plan(d: int, q: int, N: int, mu: float = 1.0, lp0: bool = False, c_delta: float = 0.0, c_M: float = 0.0,
+               mem_bytes: float = 0.0) -> dict:
+    """The paper's §4.3 parameter calibration (include/srmdp.h srmdp_plan); pure host arithmetic."""
+    out = srmdp_plan_t()
+    _check(library().srmdp_plan(d, q, N, mu, 1 if lp0 else 0, c_delta, c_M, mem_bytes, ctypes.byref(out)))
+    return {name: getattr(out, name) for name, _ in srmdp_plan_t._fields_}
 
 
 def srmdp_shard_plan(K: int, world: int, rank: int):

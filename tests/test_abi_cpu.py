@@ -132,3 +132,29 @@ def test_exchange_flag_validation_needs_no_gpu(lib):
         with pytest.raises(lib.SrmdpError) as e:
             lib.Solver(base, world=world, rank=0, flags=flags, nccl_id=b"x" * 128 if world > 1 else None)
         assert e.value.status == -1 and msg in str(e.value), (flags, str(e.value))
+
+
+def test_plan_follows_the_papers_calibration(lib):
+    """srmdp_plan (§4.3) is host arithmetic: L = log(N)/mu,
+    delta = N^{-1/4} (LP1) / N^{-1/2} (LP0) (P:815-818), #C = ceil(2L/delta),
+    M = (d+1) N^2 (LP1) / N^2 (LP0); the cost exponents of P:836-847
+    (K M N^2 ~ N^{4 + d/4} for LP1) follow from them."""
+    import math
+    p = lib.srmdp_plan(4, 4, 20, 1.0)
+    assert abs(p["L"] - math.log(20)) < 1e-15
+    assert abs(p["delta"] - 20 ** -0.25) < 1e-15
+    assert p["cells_per_dim"] == math.ceil(2 * math.log(20) / 20 ** -0.25)
+    assert p["K"] == p["cells_per_dim"] ** 4 and p["M"] == 5 * 400
+    assert p["B"] == 25 and p["B_pad"] == 48
+    assert p["path_steps"] == p["K"] * p["M"] * 20 * 21 / 2 and p["fits"] == 1
+    q = lib.srmdp_plan(4, 4, 20, 2.0, lp0=True, c_delta=0.5, c_M=2.0, mem_bytes=1e3)
+    assert abs(q["L"] - math.log(20) / 2) < 1e-15 and abs(q["delta"] - 0.5 / math.sqrt(20)) < 1e-15
+    assert q["M"] == 800 and q["fits"] == 0
+    # LP1 cost exponent: K M N(N+1)/2 grows like N^{4 + d/4} (up to the log terms of L and ceil)
+    for d in (2, 4, 8):
+        a, b = lib.srmdp_plan(d, d, 400, 1.0), lib.srmdp_plan(d, d, 6400, 1.0)
+        slope = math.log(b["path_steps"] / a["path_steps"]) / math.log(16)
+        logs = d * math.log(math.log(6400) / math.log(400)) / math.log(16)   # the (log N)^d of K
+        assert abs(slope - logs - (4 + d / 4)) < 0.1 * d / 4 + 0.05, (d, slope)
+    with pytest.raises(lib.SrmdpError):
+        lib.srmdp_plan(0, 1, 10, 1.0)
