@@ -302,7 +302,12 @@ __device__ __forceinline__ void simulate_path(const DevProblem& P, const Grid& G
                                               int64_t kl) {
   using KC = KCfg<D, Q>;
   double Xn[D];
+#ifdef SRMDP_EXPERIMENT_START_CENTER   // timing experiment only (wrong results): no start-point sampling
+#pragma unroll
+  for (int l = 0; l < D; ++l) Xn[l] = G.cen[cc[l]] + 1e-3 * (double)(m & 7);
+#else
   start_point<D, EQ>(P, G, cc, i, k, m, Xn);
+#endif
   row[0] = 1.0;
 #pragma unroll
   for (int l = 0; l < D; ++l) row[1 + l] = Xn[l] - G.cen[cc[l]];
@@ -726,6 +731,10 @@ step_kernel(const DevProblem P, const int i, const int64_t k_begin, const int64_
         }
       }
       __syncthreads();
+#ifdef SRMDP_EXPERIMENT_NO_FOLD   // timing experiment only (wrong results): no Gram / Z fold
+      if (false) {
+      } else
+#endif
       if constexpr (KC::USE_MMA && SRMDP_MMA_REUSE) {
         // fragment-reusing fold: this warp's tile row pb over its row slice
         int pb = 0;
@@ -957,13 +966,18 @@ step_kernel(const DevProblem P, const int i, const int64_t k_begin, const int64_
     __syncthreads();
 
     // ---------------- pass 2: Y responses with the fresh z_i ---
+#ifdef SRMDP_EXPERIMENT_NO_PASS2   // timing experiment only (wrong results): no pass 2 loop
+    const int64_t M2 = 0;
+#else
+    const int64_t M2 = M;
+#endif
     double ry[KC::N1];
 #pragma unroll
     for (int p = 0; p < KC::N1; ++p) ry[p] = 0.0;
 #if SRMDP_PASS2_UNROLL > 0
 #pragma unroll kPass2Unroll
 #endif
-    for (int64_t m = tid; m < M; m += kThreads) {
+    for (int64_t m = tid; m < M2; m += kThreads) {
       double a[KC::N1];
       a[0] = 1.0;
       if constexpr (store_design(D)) {

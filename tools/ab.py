@@ -30,8 +30,11 @@ def main():
     ap.add_argument("--config", default="cfg4")
     ap.add_argument("--rounds", type=int, default=4)
     ap.add_argument("--M", type=int, default=None)
+    ap.add_argument("--N", type=int, default=None, help="override N (short sweeps weigh the per-path-start work)")
     a = ap.parse_args()
     w = workloads.CONFIGS[a.config](**({"M": a.M} if a.M else {}))
+    if a.N:
+        w = dict(w, N=a.N)
     libs = []
     for p in a.libs:
         L = ctypes.CDLL(os.path.abspath(p), mode=ctypes.RTLD_LOCAL)
