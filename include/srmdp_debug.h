@@ -36,7 +36,9 @@ srmdp_status srmdp_debug_step_dump(srmdp_t* h, int i, int dump_m, uint32_t* cell
 
 /* Elementwise device detmath (docs/detmath.md): op 0 = dm_log(in) -> out0;
  * op 1 = dm_sincospi2(in) -> (out0 = sin, out1 = cos); op 2 = the path's
- * correctly rounded sqrt (dsqrt_inrange, valid for 2^-970 <= in < 2^1023) -> out0. */
+ * correctly rounded sqrt (dsqrt_inrange, valid for 2^-970 <= in < 2^1023) -> out0;
+ * op 3 = the start point's 1/p - 1 by the range-proved reciprocal
+ * (inv_minus_one<true>, valid for 2^-1000 <= in < 1) -> out0. */
 srmdp_status srmdp_debug_detmath(int op, size_t n, const double* in, double* out0, double* out1);
 
 /* Philox4x32-10 on the device: ctr[n][4], key[2] -> out[n][4]. */

@@ -1,7 +1,7 @@
 // debug_kernels.cuh — elementwise test-hook kernels of srmdp_debug.h
 // (non-template: included by srmdp.cu only).
 #pragma once
-#include "detmath.cuh"
+#include "problem.cuh"
 
 namespace srk {
 
@@ -17,6 +17,8 @@ __global__ void detmath_kernel(const int op, const int64_t n, const double* __re
     o0[t] = dm_log(in[t], T);
   } else if (op == 2) {
     o0[t] = dsqrt_inrange(in[t]);   // Box-Muller's sqrt (in-range inputs only)
+  } else if (op == 3) {
+    o0[t] = inv_minus_one<true>(in[t]);   // the start point's 1/p - 1 (2^-1000 <= p < 1 only)
   } else {
     double s, c;
     dm_sincospi2(in[t], T, s, c);

@@ -751,6 +751,12 @@ extern "C" srmdp_status srmdp_create(const srmdp_config* cfg, srmdp_t** out) {
   P.inv_delta = (double)h->C / (2.0 * cfg->L);
   P.delta = (2.0 * cfg->L) / (double)h->C;     // as grid_tables (centers)
   P.half_delta = P.delta * 0.5;
+  {   // the smallest start-point p of the grid is Fe[c] + U (Fe[c+1] - Fe[c]) >= 2^-53 min_c(Fe[c+1] - Fe[c])
+      // for the leftmost cell (Fe[0] = 0), >= Fe[1] for the others: the fast 1/p is exact above 2^-1000
+    double mind = 1.0;
+    for (int c = 0; c < h->C; ++c) mind = std::min(mind, tabs[c + 1] - tabs[c]);
+    P.rcp_fast = (mind > 0x1p-946) ? 1 : 0;
+  }
   P.neg_inv_mu = -(1.0 / cfg->mu);
   P.C_y = h->C_y; P.C_z = h->C_z;
   P.f_a = (cfg->driver.kind == SRMDP_F_LINEAR) ? cfg->driver.params[0] : 0.0;
@@ -1407,7 +1413,7 @@ extern "C" srmdp_status srmdp_debug_step_dump(srmdp_t* h, int i, int dump_m, uin
 }
 
 extern "C" srmdp_status srmdp_debug_detmath(int op, size_t n, const double* in, double* out0, double* out1) {
-  if (op < 0 || op > 2 || !in || !out0 || (op == 1 && !out1)) return SRMDP_E_ARG;
+  if (op < 0 || op > 3 || !in || !out0 || (op == 1 && !out1)) return SRMDP_E_ARG;
   if (n == 0) return SRMDP_OK;
   double* d = nullptr;
   cudaError_t e = cudaMalloc(&d, (3 * n + 512) * sizeof(double));
