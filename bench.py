@@ -284,6 +284,12 @@ def run_secondary(w, args, rank, world, local, dev, stream, fresh_nccl_id, barri
                          "executed_tflops": ex_tf, "executed_frac": (ex_tf / peak) if ex_tf else None,
                          "flops_per_path_step": flops_per_path_step(w), "flops_per_path_start": flops_per_path_start(w)},
             "hbm": hbm, "gather": gather_block(w, value), "clocks": clk.summary(),
+            # the same workload in the paper (table:LP1d15_19: d = 19, N = 5, #C = 2, M = 3200):
+            # 4370.31 s on a GTX TITAN Black in fp32 -> 5.76e6 path-steps/s (context,
+            # other hardware and precision)
+            "paper_context": {"line": "PAPER.md:1259", "gpu": "GeForce GTX TITAN Black (Kepler), fp32",
+                              "seconds": 4370.31, "path_steps_per_s": 5.76e6,
+                              "ratio": value / 5.76e6 if (w["d"], w["N"], w["C"], w["M"]) == (19, 5, 2, 3200) else None},
             "lp0_fallbacks": st["lp0_fallbacks"],
             "launch": {"grid": st["grid"], "block": st["block"], "smem_bytes": st["smem_bytes"],
                        "ctas_per_sm": st["ctas_per_sm"]}}
