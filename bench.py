@@ -419,7 +419,7 @@ def main():
             "flops_per_path_step": flops_per_path_step(w),
             "flops_per_path_start": flops_per_path_start(w),
             "kernel_share_of_step": kern_ms / total_ms, "avg_launch_ms": kern_ms / (args.steps * max(1, launches_per_solve))}
-    gather_ms = float(st["gather_ms"]) / args.steps if world > 1 or args.exchange != "nccl" else 0.0
+    gather_ms = float(st["gather_ms"]) if world > 1 or args.exchange != "nccl" else 0.0   # the last timed solve's exchange (srmdp_stats: per solve)
     solver.close()
 
     secondary = None
