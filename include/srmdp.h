@@ -125,6 +125,13 @@ typedef struct {
                                      and the multicast handle reaches the other ranks as a file descriptor
                                      over a Unix socket. SRMDP_E_UNSUPPORTED where the GPU / system has no
                                      multicast. At world == 1 the multicast object spans this GPU alone. */
+#define SRMDP_FLAG_INKERNEL_FLAGS 256 /* fused exchanges on the BM (X = W) kernels: instead of a signal and a
+                                     wait kernel after every step, the step kernel itself waits for slice
+                                     i+1 after the table-free head (start points, first increments) of
+                                     its first round -- overlapping the peers' last stores -- and its last
+                                     CTA publishes slice i. Opt-in: on one GPU the kernel is 1.4% slower
+                                     with the head / tail split compiled in, the separate kernels cost 0.35 ms
+                                     per cfg4 solve */
 #define SRMDP_FLAG_P2P_SELF_PEER 64 /* test mode of P2P_EXCHANGE at world == 1: the kernels read and store
                                      a second table on this GPU and the epilogue's peer-store loop
                                      (n_peers = 1) writes every block into the handle's own table, the

@@ -6,17 +6,17 @@
 
 using namespace srk;
 
-template <int D, int Q, bool EQ, int DK = -1>
+template <int D, int Q, bool EQ, int DK = -1, bool XW = false>
 static cudaError_t prepare_impl(int C, size_t* smem, int* ctas) {
   *smem = SmemLayout<D, Q>::bytes(C);
-  cudaError_t e = cudaFuncSetAttribute(step_kernel<D, Q, EQ, false, DK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)*smem);
+  cudaError_t e = cudaFuncSetAttribute(step_kernel<D, Q, EQ, false, DK, XW>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)*smem);
   if (e != cudaSuccess) return e;
-  return fit_carveout((const void*)step_kernel<D, Q, EQ, false, DK>, *smem, kThreads, ctas);
+  return fit_carveout((const void*)step_kernel<D, Q, EQ, false, DK, XW>, *smem, kThreads, ctas);
 }
-template <int D, int Q, bool EQ, int DK = -1>
+template <int D, int Q, bool EQ, int DK = -1, bool XW = false>
 static void step_impl(const DevProblem& P, int i, int64_t kb, int64_t nk, int grid, size_t smem, cudaStream_t s) {
-  step_kernel<D, Q, EQ, false, DK><<<grid, kThreads, smem, s>>>(P, i, kb, nk);
+  step_kernel<D, Q, EQ, false, DK, XW><<<grid, kThreads, smem, s>>>(P, i, kb, nk);
 }
 template <int D, int Q>
 static void step_dump_impl(const DevProblem& P, int i, int64_t kb, int64_t nk, int grid, size_t smem, cudaStream_t s) {
@@ -46,16 +46,19 @@ Ops make_ops() {
   void (*sd)(const DevProblem&, int, int64_t, int64_t, int, size_t, cudaStream_t) = nullptr;
   if constexpr (dump) sd = step_dump_impl<D, Q>;
   // BM-specialised kernel for the q = d benchmark dynamics (X = W)
-  cudaError_t (*pb)(int, size_t*, int*) = nullptr;
+  cudaError_t (*pb)(int, size_t*, int*) = nullptr, (*pbx)(int, size_t*, int*) = nullptr;
   void (*sb)(const DevProblem&, int, int64_t, int64_t, int, size_t, cudaStream_t) = nullptr;
+  void (*sbx)(const DevProblem&, int, int64_t, int64_t, int, size_t, cudaStream_t) = nullptr;
   if constexpr (D == Q) {
     pb = prepare_impl<D, Q, false, DYN_BM>;
     sb = step_impl<D, Q, false, DYN_BM>;
+    pbx = prepare_impl<D, Q, false, DYN_BM, true>;
+    sbx = step_impl<D, Q, false, DYN_BM, true>;
   }
   if constexpr (D <= 8)
     return Ops{D, Q, prepare_impl<D, Q, false>, step_impl<D, Q, false>, prepare_impl<D, Q, true>, step_impl<D, Q, true>,
-               eval_impl<D, Q>, trace_impl<D, Q>, sd, pb, sb};
+               eval_impl<D, Q>, trace_impl<D, Q>, sd, pb, sb, pbx, sbx};
   else
     return Ops{D, Q, prepare_impl<D, Q, false>, step_impl<D, Q, false>, nullptr, nullptr, eval_impl<D, Q>,
-               trace_impl<D, Q>, sd, pb, sb};
+               trace_impl<D, Q>, sd, pb, sb, pbx, sbx};
 }

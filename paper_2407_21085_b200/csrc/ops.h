@@ -40,6 +40,9 @@ struct Ops {
   // the equal-size-grid kernel with the dynamics fixed to BM (X = W, the §5.1 benchmark)
   cudaError_t (*prepare_bm)(int C, size_t* smem, int* ctas);
   void (*step_bm)(const srk::DevProblem&, int, int64_t, int64_t, int, size_t, cudaStream_t);
+  // the same with the in-kernel exchange flags (fused P2P / NVLS exchange)
+  cudaError_t (*prepare_bm_xw)(int C, size_t* smem, int* ctas);
+  void (*step_bm_xw)(const srk::DevProblem&, int, int64_t, int64_t, int, size_t, cudaStream_t);
 };
 
 template <int D, int Q>

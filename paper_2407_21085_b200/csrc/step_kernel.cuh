@@ -296,12 +296,11 @@ __device__ __forceinline__ void prefetch_block(const double* blk) {
 // latency, is what it costs: 256-bit instead of 128-bit loads gained 7%, an
 // explicit L1 prefetch now loses 1%. (Two paths per thread for ILP measured
 // slower: 2.43e10 vs 2.65e10.)
-template <int D, int Q, bool EQ, bool DUMP, int DK>
-__device__ __forceinline__ void simulate_path(const DevProblem& P, const Grid& G, const int (&cc)[D], int i,
-                                              uint32_t k, uint32_t m, double* row, double& Bout, double& Y1out,
-                                              int64_t kl) {
-  using KC = KCfg<D, Q>;
-  double Xn[D];
+// The table-free head of a path: start point x_i (row: 1, x_i - r_k), the
+// increments dW_i (row) and X_{i+1} = Euler(x_i, dW_i) into Xn.
+template <int D, int Q, bool EQ, int DK>
+__device__ __forceinline__ void simulate_head(const DevProblem& P, const Grid& G, const int (&cc)[D], int i,
+                                              uint32_t k, uint32_t m, double* row, double (&Xn)[D]) {
 #ifdef SRMDP_EXPERIMENT_START_CENTER   // timing experiment only (wrong results): no start-point sampling
 #pragma unroll
   for (int l = 0; l < D; ++l) Xn[l] = G.cen[cc[l]] + 1e-3 * (double)(m & 7);
@@ -320,6 +319,13 @@ __device__ __forceinline__ void simulate_path(const DevProblem& P, const Grid& G
 #pragma unroll
     for (int l = 0; l < D; ++l) Xn[l] = X1[l];
   }
+}
+
+// The rest of the path from X_{i+1} (the first gather reads slice i+1).
+template <int D, int Q, bool EQ, bool DUMP, int DK>
+__device__ __forceinline__ void simulate_tail(const DevProblem& P, const Grid& G, int i, uint32_t k, uint32_t m,
+                                              double (&Xn)[D], double& Bout, double& Y1out, int64_t kl) {
+  using KC = KCfg<D, Q>;
   double acc = 0.0, zlin = 0.0, Y1 = 0.0, yv = 0.0;
   int nexact = 0;
   const int N = P.N;
@@ -419,6 +425,15 @@ __device__ __forceinline__ void simulate_path(const DevProblem& P, const Grid& G
     if (tot && (int)(threadIdx.x & 31) == __ffs(mask) - 1) atomicAdd(P.counters + 1, (unsigned long long)tot);
   }
 #endif
+}
+
+template <int D, int Q, bool EQ, bool DUMP, int DK>
+__device__ __forceinline__ void simulate_path(const DevProblem& P, const Grid& G, const int (&cc)[D], int i,
+                                              uint32_t k, uint32_t m, double* row, double& Bout, double& Y1out,
+                                              int64_t kl) {
+  double Xn[D];
+  simulate_head<D, Q, EQ, DK>(P, G, cc, i, k, m, row, Xn);
+  simulate_tail<D, Q, EQ, DUMP, DK>(P, G, i, k, m, Xn, Bout, Y1out, kl);
 }
 
 #if SRMDP_USER_F
@@ -620,8 +635,48 @@ __device__ void chol_solve_warp(const double* L, const double* r, double* b, int
 // DUMP: debug variant (srmdp_debug_step_dump) that also writes the located
 // cells and states of the first dump_m paths of every cell; otherwise the
 // same code.
+// In-kernel exchange (XW): wait until every rank has published slice i+1
+// (flags [i+1][*] at this solve's epoch; acquire at system scope) -- one
+// thread per CTA, after the table-free head of the first round, so the start
+// points overlap the other ranks' last stores -- and, in the last CTA of the
+// launch, publish slice i (release at system scope, after every CTA's
+// stores and fence). Bounded like exchange_wait_kernel.
+__device__ __forceinline__ void xw_wait(const DevProblem& P, int slot) {
+  unsigned e;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(e) : "l"(P.xw_epoch) : "memory");
+  for (int r = 0; r < P.xw_world; ++r) {
+    const unsigned* p = P.xw_own + (size_t)slot * P.xw_world + r;
+    unsigned v;
+    for (int n = 0;; ++n) {
+      asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+      if ((int)(v - e) >= 0) break;
+      if (n > (1 << 28) || *(volatile unsigned*)P.xw_err) {   // ~minutes, or another wait already failed
+        atomicCAS(P.xw_err, 0u, 1u + (unsigned)slot);
+        return;
+      }
+      __nanosleep(200);
+    }
+  }
+}
+
+__device__ __forceinline__ void xw_signal(const DevProblem& P, int slot) {
+  __threadfence_system();
+  const unsigned e = *P.xw_epoch;
+  if (P.xw_mc) {
+    asm volatile("fence.proxy.alias;" ::: "memory");
+    unsigned* p = P.xw_mc + (size_t)slot * P.xw_world + P.xw_rank;
+    asm volatile("multimem.st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(e) : "memory");
+  } else {
+    for (int r = 0; r < P.xw_world; ++r) {
+      unsigned* p = P.xw_flags[r] + (size_t)slot * P.xw_world + P.xw_rank;
+      asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(e) : "memory");
+    }
+  }
+}
+
 // DK: dynamics family fixed at compile time (-1 = runtime, see euler()).
-template <int D, int Q, bool EQ, bool DUMP = false, int DK = -1>
+// XW: in-kernel exchange flags (above) instead of separate signal / wait kernels.
+template <int D, int Q, bool EQ, bool DUMP = false, int DK = -1, bool XW = false>
 __global__ void __launch_bounds__(kThreads, KCfg<D, Q>::CTAS)
 step_kernel(const DevProblem P, const int i, const int64_t k_begin, const int64_t nk) {
   using KC = KCfg<D, Q>;
@@ -711,13 +766,25 @@ step_kernel(const DevProblem P, const int i, const int64_t k_begin, const int64_
     for (int64_t m0 = 0; m0 < M; m0 += KC::ROWS) {
       const int nrows = (int)((M - m0) < KC::ROWS ? (M - m0) : KC::ROWS);
       const int64_t m = m0 + tid;
+      // XW: the table-free head of every path first, and in the first round
+      // of this CTA's first cell a wait for slice i+1's flags before the rest
+      // (measured: splitting every round costs less than a separate first round)
+      double Xh[D];
+      if constexpr (XW) {
+        if (m < M) simulate_head<D, Q, EQ, DK>(P, G, cc, i, k, (uint32_t)m, sRows + tid * KC::ROW, Xh);
+        if (kl == (int64_t)blockIdx.x && m0 == 0 && i < P.xw_wait_below) {
+          if (tid == 0) xw_wait(P, i + 1);
+          __syncthreads();
+        }
+      }
       if (m < M) {
         double* row = sRows + tid * KC::ROW;
         double Bv, Y1;
 #if SRMDP_USER_F
         simulate_path_user<D, Q, EQ>(P, G, cc, i, k, (uint32_t)m, row, Bv, Y1);
 #else
-        simulate_path<D, Q, EQ, DUMP, DK>(P, G, cc, i, k, (uint32_t)m, row, Bv, Y1, kl);
+        if constexpr (XW) simulate_tail<D, Q, EQ, DUMP, DK>(P, G, i, k, (uint32_t)m, Xh, Bv, Y1, kl);
+        else simulate_path<D, Q, EQ, DUMP, DK>(P, G, cc, i, k, (uint32_t)m, row, Bv, Y1, kl);
 #endif
         const double sc = Bv * P.inv_dt;
 #pragma unroll
@@ -1073,6 +1140,17 @@ step_kernel(const DevProblem P, const int i, const int64_t k_begin, const int64_
     if (P.mc_table) asm volatile("fence.proxy.alias;" ::: "memory");   // multicast alias vs the unicast reads
     if (P.n_peers || P.mc_table) __threadfence_system();   // ordered before the signal kernel's release
     __syncthreads();
+  }
+  if constexpr (XW) {
+    // the last CTA of the launch publishes slice i to every rank
+    if (tid == 0) {
+      __threadfence_system();
+      const unsigned prev = atomicAdd(P.xw_counter, 1u);
+      if (prev == gridDim.x - 1) {
+        *P.xw_counter = 0u;                  // every CTA has counted: reset for the next launch
+        xw_signal(P, i);
+      }
+    }
   }
 }
 

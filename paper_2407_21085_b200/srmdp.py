@@ -27,6 +27,7 @@ FLAG_JIT = 16
 FLAG_P2P_EXCHANGE = 32
 FLAG_P2P_SELF_PEER = 64
 FLAG_NVLS_EXCHANGE = 128
+FLAG_INKERNEL_FLAGS = 256
 
 STATUS = {0: "SRMDP_OK", -1: "SRMDP_E_ARG", -2: "SRMDP_E_PRECOND", -3: "SRMDP_E_STATE", -4: "SRMDP_E_CUDA",
           -5: "SRMDP_E_NCCL", -6: "SRMDP_E_NOMEM", -7: "SRMDP_E_UNSUPPORTED", -8: "SRMDP_E_JIT"}
