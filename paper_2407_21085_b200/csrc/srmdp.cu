@@ -515,7 +515,9 @@ static cudaError_t record_event(srmdp_t* h, cudaEvent_t e) {
 // The static kernel of this problem: the BM-specialised one for X = W on the
 // equal-size grid (the §5.1 benchmark), else the runtime-dynamics kernel.
 static bool use_bm_kernel(const srmdp_t* h) {
-  return !h->jit && !h->cfg.grid && h->cfg.dyn.kind == SRMDP_DYN_BM && h->ops->step_bm;
+  // the BM kernels compile only the range-proved start-point reciprocal (SRMDP_BM_FAST_ONLY)
+  return !h->jit && !h->cfg.grid && h->cfg.dyn.kind == SRMDP_DYN_BM && h->ops->step_bm &&
+         (!SRMDP_BM_FAST_ONLY || h->dp.rcp_fast);
 }
 
 // Fused exchanges on the BM kernels, opt-in (SRMDP_FLAG_INKERNEL_FLAGS): the
@@ -695,6 +697,13 @@ extern "C" srmdp_status srmdp_create(const srmdp_config* cfg, srmdp_t** out) {
 
   const size_t table_bytes = (size_t)h->N * h->K_pad * h->B_pad * sizeof(double);
   std::vector<double> tabs = grid_tables(h->C, cfg->L, cfg->mu, cfg->grid != 0);
+  {   // the smallest start-point p of the grid is Fe[c] + U (Fe[c+1] - Fe[c]) >= 2^-53 min_c(Fe[c+1] - Fe[c])
+      // for the leftmost cell (Fe[0] = 0), >= Fe[1] for the others: the fast 1/p is exact above 2^-1000
+      // (decided before prepare_step: the BM kernels need it)
+    double mind = 1.0;
+    for (int c = 0; c < h->C; ++c) mind = std::min(mind, tabs[c + 1] - tabs[c]);
+    h->dp.rcp_fast = (mind > 0x1p-946) ? 1 : 0;
+  }
   h->p2p = cfg->flags & SRMDP_FLAG_P2P_EXCHANGE;
   h->nvls = cfg->flags & SRMDP_FLAG_NVLS_EXCHANGE;
   {   // bounded flag waits of the fused exchange (exchange_wait_kernel)
@@ -777,12 +786,7 @@ extern "C" srmdp_status srmdp_create(const srmdp_config* cfg, srmdp_t** out) {
   P.inv_delta = (double)h->C / (2.0 * cfg->L);
   P.delta = (2.0 * cfg->L) / (double)h->C;     // as grid_tables (centers)
   P.half_delta = P.delta * 0.5;
-  {   // the smallest start-point p of the grid is Fe[c] + U (Fe[c+1] - Fe[c]) >= 2^-53 min_c(Fe[c+1] - Fe[c])
-      // for the leftmost cell (Fe[0] = 0), >= Fe[1] for the others: the fast 1/p is exact above 2^-1000
-    double mind = 1.0;
-    for (int c = 0; c < h->C; ++c) mind = std::min(mind, tabs[c + 1] - tabs[c]);
-    P.rcp_fast = (mind > 0x1p-946) ? 1 : 0;
-  }
+
   P.neg_inv_mu = -(1.0 / cfg->mu);
   P.C_y = h->C_y; P.C_z = h->C_z;
   P.f_a = (cfg->driver.kind == SRMDP_F_LINEAR) ? cfg->driver.params[0] : 0.0;

@@ -41,6 +41,9 @@ constexpr int kJUnroll = SRMDP_J_UNROLL;
 #ifndef SRMDP_LOCATE_MAGIC
 #define SRMDP_LOCATE_MAGIC 0
 #endif
+#ifndef SRMDP_BM_FAST_ONLY
+#define SRMDP_BM_FAST_ONLY 0   // 1: BM kernels compile only the range-proved start point (launched only when rcp_fast; measured neutral)
+#endif
 #ifndef SRMDP_MMA_REUSE
 #define SRMDP_MMA_REUSE 0
 #endif
@@ -305,7 +308,7 @@ __device__ __forceinline__ void simulate_head(const DevProblem& P, const Grid& G
 #pragma unroll
   for (int l = 0; l < D; ++l) Xn[l] = G.cen[cc[l]] + 1e-3 * (double)(m & 7);
 #else
-  start_point<D, EQ>(P, G, cc, i, k, m, Xn);
+  start_point<D, EQ, (DK == DYN_BM && SRMDP_BM_FAST_ONLY) ? 1 : 0>(P, G, cc, i, k, m, Xn);
 #endif
   row[0] = 1.0;
 #pragma unroll
