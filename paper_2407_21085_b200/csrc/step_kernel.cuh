@@ -41,6 +41,9 @@ constexpr int kJUnroll = SRMDP_J_UNROLL;
 #ifndef SRMDP_LOCATE_MAGIC
 #define SRMDP_LOCATE_MAGIC 0
 #endif
+#ifndef SRMDP_RNG_AHEAD
+#define SRMDP_RNG_AHEAD 0
+#endif
 #ifndef SRMDP_BM_FAST_ONLY
 #define SRMDP_BM_FAST_ONLY 0   // 1: BM kernels compile only the range-proved start point (launched only when rcp_fast; measured neutral)
 #endif
@@ -336,6 +339,13 @@ __device__ __forceinline__ void simulate_tail(const DevProblem& P, const Grid& G
 #define SRMDP_J_UNROLL_HD 1
 #endif
   constexpr int JU = (D <= 8) ? kJUnroll : SRMDP_J_UNROLL_HD;
+  // RNG one step ahead (SRMDP_RNG_AHEAD, phase-ordered Brownian only): the
+  // Philox words of step j+2 are drawn while step j+1's are transformed
+  constexpr bool AHEAD = SRMDP_RNG_AHEAD && ((Q + 1) / 2 <= SRMDP_PHASE_MAX);
+  U4 onx[(Q + 1) / 2];
+  if constexpr (AHEAD) {
+    if (i + 1 < N) brownian_words<Q>(P, i, i + 1, k, m, onx);
+  }
 #pragma unroll JU
   for (int j = i; j < N; ++j) {
     // Xn = X_{j+1}
@@ -391,7 +401,15 @@ __device__ __forceinline__ void simulate_tail(const DevProblem& P, const Grid& G
       double Xnn[D];
       {
         double dW[Q];
-        brownian<Q>(P, G, i, j + 1, k, m, dW);   // increments of step j+1
+        if constexpr (AHEAD) {
+          U4 ocur[(Q + 1) / 2];
+#pragma unroll
+          for (int b = 0; b < (Q + 1) / 2; ++b) ocur[b] = onx[b];
+          if (j + 2 < N) brownian_words<Q>(P, i, j + 2, k, m, onx);
+          brownian_transform<Q>(P, G, ocur, dW);
+        } else {
+          brownian<Q>(P, G, i, j + 1, k, m, dW);   // increments of step j+1
+        }
         euler<D, Q, DK>(P, (double)(j + 1) * P.dt, Xn, dW, Xnn);
       }
       double a[D + 1];
