@@ -230,6 +230,14 @@ static std::vector<double> grid_tables(int C, double L, double mu, bool equi) {
     t[c] = host_F(mu, e);
   }
   const double* edge = t.data() + C + 1;
+  for (int c = 0; c < C; ++c) {   // the certain-membership band and the clamp below e_{c+1} (problem.cuh)
+    const double lo = edge[c], hi = edge[c + 1];
+    const double m = 0x1p-40 * (std::fabs(L) + std::fabs(std::isfinite(lo) ? lo : 0.0) +
+                                std::fabs(std::isfinite(hi) ? hi : 0.0) + 1.0);
+    t[3 * C + 2 + c] = std::isfinite(lo) ? lo + m : lo;
+    t[4 * C + 2 + c] = std::isfinite(hi) ? hi - m : hi;
+    t[5 * C + 2 + c] = std::nextafter(hi, -INFINITY);
+  }
   for (int c = 0; c < C; ++c) {
     double r;
     if (C == 1) r = 0.0;

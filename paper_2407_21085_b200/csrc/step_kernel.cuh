@@ -309,7 +309,8 @@ __device__ __forceinline__ void simulate_head(const DevProblem& P, const Grid& G
                                               uint32_t k, uint32_t m, double* row, double (&Xn)[D]) {
 #ifdef SRMDP_EXPERIMENT_START_CENTER   // timing experiment only (wrong results): no start-point sampling
 #pragma unroll
-  for (int l = 0; l < D; ++l) Xn[l] = G.cen[cc[l]] + 1e-3 * (double)(m & 7);
+  for (int l = 0; l < D; ++l)   // a point inside the cell: the centre, or +-0.8 for the two-cell grid (centres 0)
+    Xn[l] = (P.C == 2 ? (cc[l] == 0 ? -0.8 : 0.8) : G.cen[cc[l]]) + 1e-3 * (double)(m & 7);
 #else
   start_point<D, EQ, (DK == DYN_BM && SRMDP_BM_FAST_ONLY) ? 1 : 0>(P, G, cc, i, k, m, Xn);
 #endif
