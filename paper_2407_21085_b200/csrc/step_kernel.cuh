@@ -233,6 +233,9 @@ __device__ __forceinline__ double zlin_exact(const DevProblem& P, const double* 
 // of the hot loop; measured: atomic 4.72e9, register count 4.33e9, none
 // 5.05e9 path-steps/s at cfg5). 1 = a warp-aggregated atomic inside the exact
 // branch, 2 = a per-thread register count flushed once per path.
+#ifndef SRMDP_GATHER_EL
+#define SRMDP_GATHER_EL 0   // experiment (d > 8): L2 evict_last fraction of the hot-line loads, in tenths
+#endif
 #ifndef SRMDP_COUNT_EXACT
 #define SRMDP_COUNT_EXACT 1
 #endif
@@ -248,6 +251,15 @@ __device__ __forceinline__ void eval_block(const DevProblem& P, const double* __
 #pragma unroll
   for (int u = 0; u < (NHOT + 3) / 4; ++u) {
     double v[4];
+#if SRMDP_GATHER_EL
+    if constexpr (D > 8) {
+      // experiment: L2 evict_last policy on the hot lines (a fraction of them)
+      uint64_t pol;
+      asm("createpolicy.fractional.L2::evict_last.b64 %0, %1;" : "=l"(pol) : "f"(SRMDP_GATHER_EL / 10.0f));
+      asm("ld.global.nc.L2::cache_hint.v4.f64 {%0,%1,%2,%3}, [%4], %5;"
+          : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3]) : "l"(blk + 4 * u), "l"(pol));
+    } else
+#endif
     asm("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];"
         : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3]) : "l"(blk + 4 * u));
 #pragma unroll
