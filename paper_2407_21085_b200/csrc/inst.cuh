@@ -12,11 +12,11 @@ static cudaError_t prepare_impl(int C, size_t* smem, int* ctas) {
   cudaError_t e = cudaFuncSetAttribute(step_kernel<D, Q, EQ, false, DK, XW>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)*smem);
   if (e != cudaSuccess) return e;
-  return fit_carveout((const void*)step_kernel<D, Q, EQ, false, DK, XW>, *smem, kThreads, ctas);
+  return fit_carveout((const void*)step_kernel<D, Q, EQ, false, DK, XW>, *smem, step_threads(D), ctas);
 }
 template <int D, int Q, bool EQ, int DK = -1, bool XW = false>
 static void step_impl(const DevProblem& P, int i, int64_t kb, int64_t nk, int grid, size_t smem, cudaStream_t s) {
-  step_kernel<D, Q, EQ, false, DK, XW><<<grid, kThreads, smem, s>>>(P, i, kb, nk);
+  step_kernel<D, Q, EQ, false, DK, XW><<<grid, step_threads(D), smem, s>>>(P, i, kb, nk);
 }
 template <int D, int Q>
 static void step_dump_impl(const DevProblem& P, int i, int64_t kb, int64_t nk, int grid, size_t smem, cudaStream_t s) {
@@ -24,7 +24,7 @@ static void step_dump_impl(const DevProblem& P, int i, int64_t kb, int64_t nk, i
   if (cudaFuncSetAttribute(step_kernel<D, Q, false, true, DYN_BM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)smem) != cudaSuccess)
     return;   // the launch below then fails and cudaGetLastError reports it
-  step_kernel<D, Q, false, true, DYN_BM><<<grid, kThreads, smem, s>>>(P, i, kb, nk);
+  step_kernel<D, Q, false, true, DYN_BM><<<grid, step_threads(D), smem, s>>>(P, i, kb, nk);
 }
 template <int D, int Q>
 static void eval_impl(const DevProblem& P, int i, int64_t n, const double* x, double* y, double* z, cudaStream_t s) {

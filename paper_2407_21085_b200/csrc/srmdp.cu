@@ -546,7 +546,7 @@ static cudaError_t prepare_step(srmdp_t* h) {
   h->smem = step_smem_bytes(h->d, h->q, h->C);
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)h->smem);
   if (e != cudaSuccess) return e;
-  return fit_carveout(k, h->smem, kThreads, &h->ctas);
+  return fit_carveout(k, h->smem, step_threads(h->d), &h->ctas);
 }
 
 static void launch_step(srmdp_t* h, int i, int64_t kb, int64_t nk) {
@@ -563,7 +563,7 @@ static void launch_step(srmdp_t* h, int i, int64_t kb, int64_t nk) {
     return;
   }
   void* args[] = {&h->dp, &i, &kb, &nk};
-  cudaLaunchKernel((const void*)h->jit->step[h->cfg.grid ? 1 : 0], dim3(h->grid), dim3(kThreads), args, h->smem,
+  cudaLaunchKernel((const void*)h->jit->step[h->cfg.grid ? 1 : 0], dim3(h->grid), dim3(step_threads(h->d)), args, h->smem,
                    h->stream);   // errors surface through cudaGetLastError below
 }
 
@@ -765,7 +765,7 @@ extern "C" srmdp_status srmdp_create(const srmdp_config* cfg, srmdp_t** out) {
 
   // launch configuration: persistent CTAs; the pass-2 records go to a per-CTA
   // global scratch so shared memory stays small and the L1 keeps room for the
-  // gathered coefficient lines (3 CTAs/SM at d <= 8, 2 above)
+  // gathered coefficient lines (3 x 256 threads per SM at d <= 8, 4 x 128 above)
   e = prepare_step(h);
   if (e != cudaSuccess || h->ctas < 1) {
     if (e == cudaSuccess) h->err = "step kernel does not fit on an SM";
@@ -1347,7 +1347,7 @@ extern "C" srmdp_status srmdp_stats(const srmdp_t* h, srmdp_stats_t* out) {
   s.C_z = h->C_z;
   s.K = h->K; s.K_pad = h->K_pad; s.chunk = h->chunk; s.k_begin = h->k_begin; s.k_end = h->k_end;
   s.B = h->B; s.B_pad = h->B_pad;
-  s.grid = h->grid; s.block = kThreads; s.smem_bytes = (int)h->smem; s.ctas_per_sm = h->ctas;
+  s.grid = h->grid; s.block = step_threads(h->d); s.smem_bytes = (int)h->smem; s.ctas_per_sm = h->ctas;
   *out = s;
   return SRMDP_OK;
 }

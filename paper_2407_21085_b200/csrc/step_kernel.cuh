@@ -25,10 +25,17 @@
 
 namespace srk {
 
+// Threads per CTA = paths per round. d > 8: 128-thread CTAs, 4 per SM (the
+// same 16 warps per SM at 128 registers as 2 x 256, in finer units: fewer
+// warps wait at each round's barriers; cfg5 +5.5%). d <= 8: 256 x 3 (128 x 6
+// measured -1.1% at cfg4).
 #ifndef SRMDP_THREADS
-#define SRMDP_THREADS 256   // threads per CTA = paths per round (A/B: build.py -DSRMDP_THREADS=128)
+#define SRMDP_THREADS 256
 #endif
-constexpr int kThreads = SRMDP_THREADS;
+#ifndef SRMDP_THREADS_HI
+#define SRMDP_THREADS_HI 128
+#endif
+__host__ __device__ constexpr int step_threads(int d) { return d > 8 ? SRMDP_THREADS_HI : SRMDP_THREADS; }
 
 // Kernel variants (A/B builds: build.py -DNAME=VALUE)
 #ifndef SRMDP_LDG256
@@ -89,11 +96,12 @@ __host__ __device__ constexpr int row_stride(int d, int q) { return (1 + d + q) 
 // (+8 doubles: the MMA fragment loads of the last row read up to 7 padding
 // columns past the tile; they only feed discarded outputs)
 __host__ __device__ constexpr size_t step_smem_bytes(int d, int q, int C) {
-  return sizeof(double) * (size_t)((smem_tabs_len(d, C) + kThreads * row_stride(d, q) + 8 + 1) & ~1);
+  return sizeof(double) * (size_t)((smem_tabs_len(d, C) + step_threads(d) * row_stride(d, q) + 8 + 1) & ~1);
 }
 
 template <int D, int Q>
 struct KCfg {
+  static constexpr int kThreads = step_threads(D);
   static constexpr int N1 = D + 1;
   static constexpr int NB = (Q + 1) * N1;           // B
   static constexpr int NH = hot_len(D);             // hot part [Y | W | S | pad]
@@ -102,13 +110,14 @@ struct KCfg {
   static constexpr int NZ = Q * N1;                 // Z right-hand-side entries
   static constexpr int E = NG + NZ;
   static constexpr int ROWS = kThreads;            // rows (paths) per round: one path per thread
-  // resident CTAs per SM (launch bounds): 3 (<= 85 registers) up to d = 8; the
-  // high-d kernels keep their d-long state in 128 registers at 2 CTAs/SM
+  // resident CTAs per SM (launch bounds): 3 x 256 threads (<= 85 registers) up
+  // to d = 8; the high-d kernels keep their d-long state in 128 registers at
+  // 4 x 128 threads per SM
 #ifndef SRMDP_CTAS_LO
 #define SRMDP_CTAS_LO 3
 #endif
 #ifndef SRMDP_CTAS_HI
-#define SRMDP_CTAS_HI 2
+#define SRMDP_CTAS_HI 4
 #endif
   static constexpr int CTAS = (D > 8) ? SRMDP_CTAS_HI : SRMDP_CTAS_LO;
   static constexpr int S = (E <= kThreads) ? (kThreads / E) : 1;  // row slices per entry
@@ -178,6 +187,7 @@ struct SmemLayout {
   // d = 6 CTA at 31 KB, so 3 CTAs/SM fit a 100 KB shared-memory carveout and
   // L1 keeps the rest for the coefficient hot lines (fit_carveout, ops.h).
   using KC = KCfg<D, Q>;
+  static constexpr int kThreads = KC::kThreads;
   static constexpr int MMA_RED = (SRMDP_MMA_REUSE ? KC::RSLOTS : KC::ITEMS) * 64;
   static constexpr int RED = (((KC::USE_MMA ? MMA_RED : KC::PAIRS) > kThreads
                                    ? (KC::USE_MMA ? MMA_RED : KC::PAIRS)
@@ -728,9 +738,10 @@ __device__ __forceinline__ void xw_signal(const DevProblem& P, int slot) {
 // DK: dynamics family fixed at compile time (-1 = runtime, see euler()).
 // XW: in-kernel exchange flags (above) instead of separate signal / wait kernels.
 template <int D, int Q, bool EQ, bool DUMP = false, int DK = -1, bool XW = false>
-__global__ void __launch_bounds__(kThreads, KCfg<D, Q>::CTAS)
+__global__ void __launch_bounds__(step_threads(D), KCfg<D, Q>::CTAS)
 step_kernel(const DevProblem P, const int i, const int64_t k_begin, const int64_t nk) {
   using KC = KCfg<D, Q>;
+  constexpr int kThreads = KC::kThreads;
   using SL = SmemLayout<D, Q>;
   extern __shared__ double sm[];
   const int C = P.C;
